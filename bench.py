@@ -1,0 +1,359 @@
+"""Benchmark: realization·timesteps/s of the noisy-CTQW hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the configuration the metric is quoted on
+that fits one GPU): 2 particles on an N = 256 ring (D = 65 536, 1 MiB complex128
+state per realization), R = 1000 realizations PER GPU (weak scaling), static
+tunnelling noise (levels +-0.1, seeds (1234, r)), Taylor order 4, dt = 0.02,
+the per-step norm policy, and one collection point (diagonal observables:
+populations, position moments, participation ratio) at the end of the timed
+region (post_rate = K).  A "step" advances every realization by one dt.
+
+Lines printed by rank 0 (one JSON object):
+  value       realization·steps/s over all ranks, device-timed (CUDA events,
+              max over ranks), states resident in HBM (1 GiB per buffer >> L2)
+  e2e         the same metric through the public API ``run(config)``: host
+              initial state uploaded, noise drawn, K steps, observable rows
+              copied back to the host, wall-timed
+  roofline    the streaming step kernel: algorithmic bytes 32*D per
+              realization per launch / CUDA-event launch time, vs MEASURED_PEAKS
+  cpu_baseline the NumPy oracle port on the host cores, bounded sample
+``--impl reference`` runs the reference algorithm (oracle port of
+``ctqw._evolve_segment``) on the host cores on a bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "realization·timesteps/sec (2-particle, N-site lattice)"
+UNIT = "realization·steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--m", type=int, default=2)
+    ap.add_argument("--realizations", type=int, default=1000, help="per GPU")
+    ap.add_argument("--backend", default="taylor", choices=("taylor", "rk4"))
+    ap.add_argument("--order", type=int, default=4)
+    ap.add_argument("--dt", type=float, default=0.02)
+    ap.add_argument("--fma", action="store_true", help="FMA-contracted stencil instead of exact order")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle port = the reference's algorithm, NumPy)
+
+
+def _cpu_worker(args):
+    n, m, count, r0, steps, dt, backend, order = args
+    import numpy as np
+
+    from oracle import ctqw_oracle as orc
+
+    noise = np.stack([np.random.default_rng((1234, r)).choice(np.array([-0.1, 0.1]), n)
+                      for r in range(r0, r0 + count)])
+    st = orc.make_stencil(m, n, 0.0, 1.0, 0.0, link=noise, batch=count)
+    psi = np.tile(orc.product_state(m, n), (count, 1))
+    t0 = time.perf_counter()
+    orc.evolve_segment(st, psi, 0, steps, dt, 1.0, backend, order)
+    return time.perf_counter() - t0
+
+
+def cpu_rate(n, m, backend, order, dt, per_core, steps, cores=None):
+    """Wall rate of the oracle on ``cores`` processes (OPENBLAS 1 thread each)."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+
+    cores = cores or host_cores()
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    jobs = [(n, m, per_core, 100000 + i * per_core, steps, dt, backend, order) for i in range(cores)]
+    with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as pool:
+        list(pool.map(_cpu_worker, [(n, m, 1, 0, 1, dt, backend, order)] * cores))  # warm imports
+        t0 = time.perf_counter()
+        list(pool.map(_cpu_worker, jobs))
+        wall = time.perf_counter() - t0
+    return cores * per_core * steps / wall, cores, wall
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_sample_size(n, m, seconds, cores):
+    """Realizations per core and steps so the sample takes ~``seconds``."""
+    dim = n ** m
+    per_rstep = 1.2e-7 * dim * 4  # ~0.12 us per element per Taylor order (order of magnitude)
+    steps = 4
+    per_core = max(1, int(seconds / (per_rstep * steps)))
+    return min(per_core, 16), steps
+
+
+def reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = host_cores()
+    per_core, _ = cpu_sample_size(a.n, a.m, 2.0, cores)
+    per_core = max(1, min(per_core, 4))
+    rates = []
+    for _ in range(a.warmup):
+        cpu_rate(a.n, a.m, a.backend, a.order, a.dt, per_core, 1, cores)
+    t_all = 0.0
+    for _ in range(a.steps):
+        r, _, wall = cpu_rate(a.n, a.m, a.backend, a.order, a.dt, per_core, 1, cores)
+        rates.append(r)
+        t_all += wall
+    value = a.steps * cores * per_core / t_all
+    sample = f"{cores} processes x {per_core} realizations x 1 step per timed step (N={a.n}, m={a.m})"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * t_all / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+        "data": "synthetic (static tunnelling noise, seeds (1234, r))",
+        "config": workload_config(a),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(a):
+    return {
+        "workload": f"configs[1]: m={a.m} particles, N={a.n} ring (D={a.n ** a.m}), "
+                    f"{a.realizations} realizations per GPU, static tunnelling noise, "
+                    f"{a.backend}{'' if a.backend == 'rk4' else '-' + str(a.order)}, dt={a.dt}, "
+                    f"norm policy every step, diagonal observables at the last step",
+        "n_sites": a.n, "particles": a.m, "realizations_per_gpu": a.realizations,
+        "backend": a.backend, "taylor_order": a.order, "dt": a.dt,
+        "exact_order": not a.fma,
+        "l2_policy": "inputs larger than L2 (state stack 1 GiB per buffer per GPU)",
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1612_00746_b200 as p
+    from paper_1612_00746_b200 import engine, sharding
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    R_total = a.realizations * world
+    obs = ("populations", "position_mean_variance", "participation_ratio")
+    cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([a.n]), a.m),
+                      noise=p.NoiseSpec(target="tunneling", levels=(-0.1, 0.1), rate=0.0),
+                      stepper=p.StepperConfig(backend=a.backend, dt=a.dt, taylor_order=a.order),
+                      realizations=R_total, steps=a.steps, post_rate=a.steps, precision="double",
+                      observables=obs, memory_budget=170 * 2**30, exact=not a.fma, device=local)
+    lo, hi = sharding.shard_bounds(R_total, world, rank)
+    ens = engine.EnsembleState(cfg, local, lo, hi)
+    h = ens.handle
+    dim = a.n ** a.m
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (includes one collection point)
+    for k in range(a.warmup):
+        ens.evolve(k, 1)
+        ens.stats()
+    engine.collect_observables(cfg, ens)
+    torch.cuda.synchronize()
+
+    # timed region: K steps + the collection point, device-timed
+    ens.handle.kernel_timing(True)
+    launches0 = h.launches
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record()
+        ens.evolve(a.warmup, a.steps)
+        stats = ens.stats()
+        engine.collect_observables(cfg, ens)
+        stop.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(stop)
+    kernel_ms, kernel_launches = h.kernel_time()
+    h.kernel_timing(False)
+    launches = h.launches - launches0
+    t = torch.tensor([ms], device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = R_total * a.steps / (ms_max / 1000.0)
+    assert stats["failure"] is None
+
+    # roofline of the dominant kernel (streaming step / resident segment)
+    avg_launch_ms = kernel_ms / max(kernel_launches, 1)
+    bytes_per_launch = (hi - lo) * 32.0 * dim
+    if kernel_launches == 1 and a.n <= 64:
+        bytes_per_launch *= a.steps  # resident: one launch covers every step
+    achieved = bytes_per_launch / (avg_launch_ms / 1000.0) / 1e9
+    peak, peak_src = measured_peak_hbm()
+    traffic = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                "kernel": "tile_step_kernel" if a.n > 64 else "resident_kernel",
+                "kernel_ms_avg": avg_launch_ms, "kernel_launches": kernel_launches,
+                "kernel_share_of_step": kernel_ms / ms if ms > 0 else None,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
+                "flops_per_launch": (hi - lo) * dim * (22.0 * a.order if a.backend == "taylor" else 112.0)}
+    roofline["achieved_fp64_tflops"] = roofline["flops_per_launch"] / (avg_launch_ms / 1000.0) / 1e12
+
+    # e2e through the public API: run(config) with host I/O
+    e2e = None
+    if not a.no_e2e:
+        sinks = p.MemorySinks(keep_densities=False)
+        barrier()
+        t0 = time.perf_counter()
+        p.run(cfg, sinks, group=None if world == 1 else dist.group.WORLD)
+        torch.cuda.synchronize()
+        t_e2e = torch.tensor([time.perf_counter() - t0], device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e_s = float(t_e2e.item())
+        h2d = dim * 16 + 16  # initial state + noise levels
+        d2h = (a.n + 3) * 8 * len(cfg.schedule)  # observable rows per collection point
+        e2e = {"value": R_total * a.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": h2d / a.steps, "d2h_bytes_per_step": d2h / a.steps,
+               "seconds": e2e_s, "api": "paper_1612_00746_b200.run(RunConfig, MemorySinks)"}
+
+    cpu = None
+    if rank == 0 and not a.no_cpu:
+        cores = host_cores()
+        per_core, steps = cpu_sample_size(a.n, a.m, a.cpu_seconds, cores)
+        rate, cores, wall = cpu_rate(a.n, a.m, a.backend, a.order, a.dt, per_core, steps, cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{cores} processes x {per_core} realizations x {steps} steps of the same "
+                         f"workload (oracle port of the reference algorithm), {wall:.1f} s wall"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic (static tunnelling noise drawn on device, seeds (1234, r))",
+            "config": dict(workload_config(a), parallelism=f"realizations sharded over {world} GPU(s)"),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "norm_events": stats["event_count"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        reference_arm(a)
+    else:
+        ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * ctqw.h -- C ABI of libctqw.so, the B200 (sm_100a) hot path of the noisy
+ * many-particle continuous-time-quantum-walk ensemble simulator.
+ *
+ * Plain C: pointers, sizes, POD structs.  No torch or C++ types cross the
+ * boundary, no exceptions, no allocations handed to the caller.  Device
+ * pointers (suffix _dev) are caller-owned CUDA allocations on the handle's
+ * device (torch tensors in the Python host layer); the library keeps only
+ * its own scratch and statistics buffers.  Streams are passed as void*
+ * (a cudaStream_t); NULL means the legacy default stream.
+ *
+ * Every entry point returns a status equal to the reference's
+ * CtqwError.exit_code (pkg/src/ctqw/errors.py:8-75):
+ *   0 ok, 2 configuration, 3 numeric (norm failure), 4 capacity, 1 other
+ *   (CUDA failure).  ctqw_last_error() gives the message.
+ *
+ * The reference (pkg/src/ctqw, pure Python/NumPy) has no FFI of its own;
+ * each entry point below names the Python function whose contract it takes
+ * over.  States are complex128 stored as interleaved (re, im) doubles,
+ * realization-major, each realization a row-major N^m joint vector with
+ * particle 0 the most significant digit (hilbert.py:141-159).
+ */
+#ifndef CTQW_H
+#define CTQW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTQW_ABI_VERSION 1
+
+#define CTQW_OK 0
+#define CTQW_ERR_OTHER 1
+#define CTQW_ERR_CONFIG 2
+#define CTQW_ERR_NUMERIC 3
+#define CTQW_ERR_CAPACITY 4
+
+#define CTQW_BACKEND_TAYLOR 0
+#define CTQW_BACKEND_RK4 1
+
+#define CTQW_MAX_EVENTS 100 /* ensemble.py:119 MAX_EVENTS_PER_SEGMENT */
+
+typedef struct ctqw_ctx *ctqw_handle_t;
+
+/* Geometry + deterministic couplings.  Replaces JointSpace/LatticeTopology
+ * (hilbert.py:45-138) and CouplingModel (hamiltonian.py:30-72) for the
+ * supported family: q = 1, periodic, k_half = 1, 1 <= m <= 3, n_sites >= 3. */
+typedef struct {
+  int32_t m;            /* particles */
+  int32_t n_sites;      /* ring length N */
+  int32_t k_half;       /* must be 1 */
+  int32_t periodic;     /* must be 1 */
+  double onsite_energy; /* eps0 */
+  double tunneling;     /* t */
+  double interaction;   /* U, per coinciding pair */
+  double hbar;
+} ctqw_model_t;
+
+/* Integrator + norm policy.  Mirrors StepperConfig (propagators.py:61-86). */
+typedef struct {
+  int32_t backend;     /* CTQW_BACKEND_TAYLOR / CTQW_BACKEND_RK4 */
+  int32_t order;       /* Taylor order (ignored for RK4) */
+  double dt;
+  double tol_norm;
+  double tol_fail;
+  int32_t renormalize;
+  int32_t exact;       /* 1: reference operation order, no FMA contraction
+                          (bit-identical to the reference between rescales);
+                          0: FMA-contracted stencil (<= 1e-14 from it) */
+} ctqw_stepper_t;
+
+/* NormEvent (propagators.py:89-96). */
+typedef struct {
+  double deviation;
+  int64_t realization;
+  int64_t step;
+  int32_t corrected;
+  int32_t reserved;
+} ctqw_norm_event_t;
+
+/* _SegmentStats (ensemble.py:414-423) plus the NormFailureError payload
+ * (errors.py:26-49, re-tagged as in ensemble.py:509-516). */
+typedef struct {
+  int64_t event_count;
+  int64_t corrections;
+  double max_deviation;
+  int32_t failed;
+  int32_t n_events;
+  int64_t fail_realization;
+  int64_t fail_step;
+  double fail_deviation;
+  ctqw_norm_event_t events[CTQW_MAX_EVENTS];
+} ctqw_segment_stats_t;
+
+int ctqw_abi_version(void);
+const char *ctqw_last_error(ctqw_handle_t h); /* h may be NULL */
+
+/* Bind a model to a device.  Validation follows hilbert.py:58-82,
+ * hamiltonian.py:44-63 (exit 2) and the joint-index capacity (exit 4). */
+int ctqw_create(const ctqw_model_t *model, int32_t device, ctqw_handle_t *out);
+int ctqw_destroy(ctqw_handle_t h);
+
+/* Static noise draw on the device, bit-identical to
+ * init_process(spec, lattice, seed=(master_seed, r)).values for
+ * r = r0 .. r0+count-1 (noise.py:128-159, ensemble.py:680-682):
+ * SeedSequence -> PCG64 -> Generator.choice(levels, total).
+ * noise_dev is [count][total] doubles, levels_host has n_levels entries. */
+int ctqw_draw_noise(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64_t count,
+                    const double *levels_host, int32_t n_levels, int64_t total,
+                    double *noise_dev, void *stream);
+
+/* Stencil coefficients from noise rows [links(n_links) | sites(n_sites)]:
+ * hop = t + xi_link (hamiltonian.py:137-141), site = xi_site
+ * (hamiltonian.py:134-135).  n_links is 0 or N, n_sites is 0 or N.
+ * hop_dev is [count][N]; site_dev is [count][N] and is written only when
+ * n_sites == N. */
+int ctqw_build_coefficients(ctqw_handle_t h, const double *noise_dev, int64_t count,
+                            int64_t n_links, int64_t n_sites, double *hop_dev,
+                            double *site_dev, void *stream);
+
+/* Bind coefficient rows used by every compute call below: realization i of
+ * a call reads hop_dev + i*stride (stride 0 broadcasts one Hamiltonian,
+ * like an unbatched `values` table).  site_dev NULL = no on-site noise. */
+int ctqw_bind_coefficients(ctqw_handle_t h, int64_t count, const double *hop_dev,
+                           const double *site_dev, int64_t stride);
+
+/* psi_dev[r] = psi0_dev for r < count (np.tile, ensemble.py:678). */
+int ctqw_fill_states(ctqw_handle_t h, double *psi_dev, int64_t count, const double *psi0_dev,
+                     void *stream);
+
+/* out = H psi for a batch (apply_values, hamiltonian.py:195-223). */
+int ctqw_apply(ctqw_handle_t h, const double *psi_dev, double *out_dev, int64_t count,
+               int32_t exact, void *stream);
+
+/* One propagation step with no norm policy: step_taylor_values /
+ * step_rk4_values (propagators.py:167-241).  out may not alias psi. */
+int ctqw_step(ctqw_handle_t h, const double *psi_dev, double *out_dev, int64_t count,
+              const ctqw_stepper_t *stepper, void *stream);
+
+/* check_norm_stack (propagators.py:309-328): deviations_dev[count] and
+ * corrected_dev[count] are written; the stack is rescaled in place.  On a
+ * failure returns 3 with *fail_row (argmax) and *fail_deviation set and
+ * leaves the stack untouched.  Synchronises the stream. */
+int ctqw_check_norm(ctqw_handle_t h, double *psi_dev, int64_t count,
+                    const ctqw_stepper_t *stepper, double *deviations_dev,
+                    int32_t *corrected_dev, int64_t *fail_row, double *fail_deviation,
+                    void *stream);
+
+/* The segment inner loop (_evolve_segment, ensemble.py:445-558) for static
+ * noise: n_steps steps of `count` realizations starting after step
+ * first_step, each followed by the norm policy.  work_dev is a caller-owned
+ * buffer shaped like psi_dev.  Asynchronous: the advanced stack is in
+ * psi_dev, or in work_dev when *result_in_work is set on return.  Statistics
+ * of the call are read with ctqw_segment_stats. */
+int ctqw_evolve(ctqw_handle_t h, double *psi_dev, double *work_dev, int64_t count,
+                int64_t first_step, int64_t n_steps, const ctqw_stepper_t *stepper,
+                int32_t *result_in_work, void *stream);
+
+/* Synchronise and reduce the statistics of the last ctqw_evolve call.
+ * Realization indices are offset by r0.  Returns 3 when a realization
+ * failed (the stats carry the culprit, as NormFailureError does). */
+int ctqw_segment_stats(ctqw_handle_t h, int64_t r0, ctqw_segment_stats_t *out, void *stream);
+
+/* diag_sum_dev[alpha] (+)= sum_r |psi_r(alpha)|^2, realizations summed in
+ * order (the diagonal of accumulate_density's Gram, density.py:91-92,
+ * before the division by R).  accumulate = 0 overwrites. */
+int ctqw_observe_diag(ctqw_handle_t h, const double *psi_dev, int64_t count,
+                      double *diag_sum_dev, int32_t accumulate, void *stream);
+
+/* From the (all-reduced) diagonal sum and the total realization count:
+ * populations_dev[N] (observables.py:40-56) and scalars_dev[3] =
+ * {sum_alpha p, sum_alpha p^2, participation ratio} (observables.py:94-101)
+ * with p = diag_sum / total_count.  joint_dev (optional, [N^m]) receives p. */
+int ctqw_observe_reduce(ctqw_handle_t h, const double *diag_sum_dev, double total_count,
+                        double *populations_dev, double *scalars_dev, double *joint_dev,
+                        void *stream);
+
+/* sumsq_dev[0] = sum_{i,j} |<a_i|b_j>|^2 over two state stacks: the
+ * off-diagonal information purity needs (observables.py:86-91) without the
+ * dense rho.  b_dev == a_dev uses the Hermitian symmetry. */
+int ctqw_overlap_sumsq(ctqw_handle_t h, const double *a_dev, int64_t count_a,
+                       const double *b_dev, int64_t count_b, double *sumsq_dev, void *stream);
+
+/* Kernel launches issued by this handle since creation (for bench.py). */
+int64_t ctqw_launch_count(ctqw_handle_t h);
+
+/* Timing mode (bench.py): when enabled, ctqw_evolve brackets each launch of
+ * its dominant step kernel with CUDA events on the launch stream;
+ * ctqw_kernel_time synchronises, returns the summed elapsed milliseconds and
+ * the number of bracketed launches, and clears the record. */
+int ctqw_kernel_timing(ctqw_handle_t h, int32_t enable);
+int ctqw_kernel_time(ctqw_handle_t h, double *total_ms, int64_t *launches, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CTQW_H */

@@ -1,0 +1,689 @@
+// C ABI of libctqw.so (declared in include/ctqw.h): handle management,
+// validation with the reference's error classes, and the path dispatch of
+// ctqw_evolve:
+//   m = 2, N <= 64            -> resident kernel (whole segment on chip)
+//   m = 2, N > 64, order <= 4 -> streaming tile kernel, one launch per step
+//   otherwise (m = 1, 3, ...) -> generic per-application kernels
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ctqw.h"
+#include "ctqw_device.cuh"
+#include "kernels.h"
+
+using namespace ctqw;
+
+struct ctqw_ctx {
+  int device = 0;
+  ctqw_model_t model{};
+  int m = 0, n = 0;
+  int64_t dim = 0;
+  StencilConst k{};
+  // bound coefficient rows (caller-owned)
+  int64_t coef_count = 0;
+  const double* hop = nullptr;
+  const double* site = nullptr;
+  int64_t stride = 0;
+  // library-owned device buffers
+  double* levels = nullptr;
+  int64_t levels_cap = 0;
+  double* partial = nullptr;
+  int64_t partial_cap = 0;
+  double* scl = nullptr;
+  RealStat* stats = nullptr;
+  EventRec* events = nullptr;
+  int64_t stat_cap = 0;
+  long long* fail = nullptr;
+  Summary* summary_dev = nullptr;
+  Summary* summary_host = nullptr;
+  double2* scratch[2] = {nullptr, nullptr};
+  int64_t scratch_elems = 0;
+  double* n2_dev = nullptr;
+  int64_t n2_cap = 0;
+  double* small = nullptr;  // observe_reduce scratch (2 x 148 doubles)
+  double* overlap_partial = nullptr;
+  int64_t overlap_cap = 0;
+  int64_t last_count = 0;
+  std::atomic<long long> launches{0};
+  // optional CUDA-event timing of the dominant kernel launches (bench.py)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  int64_t timed_launches = 0;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail_with(ctqw_ctx* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  g_err = msg;
+  return code;
+}
+
+int check_cuda(ctqw_ctx* h, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return CTQW_OK;
+  return fail_with(h, CTQW_ERR_OTHER, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(h, expr)                                     \
+  do {                                                        \
+    int _rc = check_cuda((h), (expr), #expr);                 \
+    if (_rc != CTQW_OK) return _rc;                           \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+int ensure(ctqw_ctx* h, T** ptr, int64_t* cap, int64_t want, const char* what) {
+  if (want <= *cap && *ptr) return CTQW_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc((void**)ptr, (size_t)std::max<int64_t>(want, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail_with(h, CTQW_ERR_CAPACITY,
+                     std::string("cannot allocate ") + what + ": " + cudaGetErrorString(e));
+  }
+  *cap = want;
+  return CTQW_OK;
+}
+
+int ensure_stats(ctqw_ctx* h, int64_t count) {
+  if (count <= h->stat_cap && h->stats) return CTQW_OK;
+  if (h->scl) cudaFree(h->scl);
+  if (h->stats) cudaFree(h->stats);
+  if (h->events) cudaFree(h->events);
+  h->scl = nullptr;
+  h->stats = nullptr;
+  h->events = nullptr;
+  h->stat_cap = 0;
+  const int64_t c = std::max<int64_t>(count, 1);
+  if (cudaMalloc((void**)&h->scl, c * sizeof(double)) != cudaSuccess ||
+      cudaMalloc((void**)&h->stats, c * sizeof(RealStat)) != cudaSuccess ||
+      cudaMalloc((void**)&h->events, c * kMaxEvents * sizeof(EventRec)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate per-realization statistics");
+  }
+  h->stat_cap = count;
+  return CTQW_OK;
+}
+
+int ensure_scratch(ctqw_ctx* h, int64_t elems) {
+  if (elems <= h->scratch_elems && h->scratch[0]) return CTQW_OK;
+  for (auto& p : h->scratch) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  h->scratch_elems = 0;
+  for (auto& p : h->scratch) {
+    if (cudaMalloc((void**)&p, (size_t)elems * sizeof(double2)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate propagation scratch");
+    }
+  }
+  h->scratch_elems = elems;
+  return CTQW_OK;
+}
+
+// Record a CUDA event on s (timing mode); returns nullptr when disabled.
+cudaEvent_t timing_event(ctqw_ctx* h, cudaStream_t s) {
+  if (!h->timing) return nullptr;
+  if (h->ev_used == h->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    h->ev_pool.push_back(e);
+  }
+  cudaEvent_t e = h->ev_pool[h->ev_used++];
+  cudaEventRecord(e, s);
+  return e;
+}
+
+int validate_stepper(ctqw_ctx* h, const ctqw_stepper_t* st) {
+  if (!st) return fail_with(h, CTQW_ERR_CONFIG, "stepper is NULL");
+  if (st->backend != CTQW_BACKEND_TAYLOR && st->backend != CTQW_BACKEND_RK4)
+    return fail_with(h, CTQW_ERR_CONFIG, "backend must be taylor or rk4 (eigen is not on the B200 path)");
+  if (!(std::isfinite(st->dt) && st->dt > 0))
+    return fail_with(h, CTQW_ERR_CONFIG, "dt must be positive and finite");
+  if (st->backend == CTQW_BACKEND_TAYLOR && (st->order < 1 || st->order > 16))
+    return fail_with(h, CTQW_ERR_CONFIG, "taylor_order must be in [1, 16] on the B200 path");
+  if (!(0 < st->tol_norm && st->tol_norm < st->tol_fail))
+    return fail_with(h, CTQW_ERR_CONFIG, "need 0 < tol_norm < tol_fail");
+  return CTQW_OK;
+}
+
+StepScalars scalars_for(const ctqw_ctx* h, const ctqw_stepper_t* st) {
+  StepScalars sc{};
+  sc.backend = st->backend;
+  // coeff = -1j*dt/hbar has real part 0 and imaginary part -dt/hbar; the
+  // Taylor recursion multiplies by coeff/j (propagators.py:185,191).
+  const double c = -st->dt / h->model.hbar;
+  if (st->backend == CTQW_BACKEND_TAYLOR) {
+    sc.order = st->order;
+    for (int j = 1; j <= st->order; ++j) sc.ci[j - 1] = c / (double)j;
+  } else {
+    sc.order = 4;
+    sc.ci[0] = c;
+  }
+  return sc;
+}
+
+Coef coef_of(const ctqw_ctx* h) { return Coef{h->hop, h->site, h->stride}; }
+
+int check_bound(ctqw_ctx* h, int64_t count) {
+  if (!h->hop) return fail_with(h, CTQW_ERR_CONFIG, "no coefficients bound (ctqw_bind_coefficients)");
+  if (count < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative realization count");
+  if (h->stride != 0 && count > h->coef_count)
+    return fail_with(h, CTQW_ERR_CONFIG, "more realizations than bound coefficient rows");
+  return CTQW_OK;
+}
+
+// One generic step (no norm policy when partial == nullptr).
+// in/out: Taylor reads `in`, writes `out` (may equal in only when scaled
+// lazily through scl and n >= 2); A/C scratch term buffers, B accumulator.
+int generic_step(ctqw_ctx* h, const ctqw_stepper_t* st, const StepScalars& sc, const double2* in,
+                 double2* out, double2* A, double2* B, double2* C, int64_t count,
+                 const double* scl, double* partial, const long long* fail, cudaStream_t s) {
+  const Coef coef = coef_of(h);
+  const bool exact = st->exact != 0;
+  const bool scale = scl != nullptr;
+  const bool inplace = (const void*)in == (const void*)out;
+  long long launches = 0;
+  const int64_t rows_chunks = (count + kMaxGridY - 1) / kMaxGridY;
+  if (sc.backend == CTQW_BACKEND_TAYLOR) {
+    const int n_ord = sc.order;
+    const double2* term_in = in;
+    double2* bufs[2] = {A, C};
+    int which = 0;
+    for (int j = 1; j <= n_ord; ++j) {
+      const bool first = j == 1, last = j == n_ord;
+      double2* term_out = last ? nullptr : bufs[which];
+      const double2* acc_in = first ? in : B;
+      double2* acc_out = (last && !(inplace && first)) ? out : B;
+      CUDA_TRY(h, launch_taylor_order(h->m, exact, first && scale, term_in, term_out, acc_in,
+                                      acc_out, count, h->dim, h->n, coef, h->k, sc.ci[j - 1],
+                                      scl, last ? partial : nullptr, fail, s));
+      launches += rows_chunks;
+      if (!last) {
+        term_in = bufs[which];
+        which ^= 1;
+      }
+    }
+    if (inplace && n_ord == 1) {
+      CUDA_TRY(h, cudaMemcpyAsync(out, B, (size_t)count * h->dim * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, s));
+    }
+  } else {
+    const double ci = sc.ci[0];
+    CUDA_TRY(h, launch_rk4_stage(h->m, exact, scale, 1, in, in, nullptr, A, B, count, h->dim,
+                                 h->n, coef, h->k, ci, scl, nullptr, fail, s));
+    CUDA_TRY(h, launch_rk4_stage(h->m, exact, scale, 2, A, in, B, C, B, count, h->dim, h->n, coef,
+                                 h->k, ci, scl, nullptr, fail, s));
+    CUDA_TRY(h, launch_rk4_stage(h->m, exact, scale, 3, C, in, B, A, B, count, h->dim, h->n, coef,
+                                 h->k, ci, scl, nullptr, fail, s));
+    CUDA_TRY(h, launch_rk4_stage(h->m, exact, false, 4, A, in, B, nullptr, out, count, h->dim,
+                                 h->n, coef, h->k, ci, scl, partial, fail, s));
+    launches += 4 * rows_chunks;
+  }
+  h->launches += launches;
+  return CTQW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ctqw_abi_version(void) { return CTQW_ABI_VERSION; }
+
+const char* ctqw_last_error(ctqw_handle_t h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
+  if (!model || !out) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL argument");
+  *out = nullptr;
+  const ctqw_model_t& md = *model;
+  if (md.m < 1 || md.m > 3)
+    return fail_with(nullptr, CTQW_ERR_CONFIG, "the B200 path supports 1 <= m <= 3 particles");
+  if (md.n_sites < 3)
+    return fail_with(nullptr, CTQW_ERR_CONFIG, "ring needs n_sites >= 3 (2*k_half < extent)");
+  if (md.k_half != 1 || md.periodic != 1)
+    return fail_with(nullptr, CTQW_ERR_CONFIG,
+                     "the B200 path supports periodic nearest-neighbour rings (k_half = 1)");
+  for (double v : {md.onsite_energy, md.tunneling, md.interaction, md.hbar})
+    if (!std::isfinite(v)) return fail_with(nullptr, CTQW_ERR_CONFIG, "model parameters must be finite");
+  if (!(md.hbar > 0)) return fail_with(nullptr, CTQW_ERR_CONFIG, "hbar must be > 0");
+  double dimd = std::pow((double)md.n_sites, md.m);
+  if (dimd > 4.0e12) return fail_with(nullptr, CTQW_ERR_CAPACITY, "joint dimension too large");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail_with(nullptr, CTQW_ERR_OTHER, "no CUDA device available");
+  }
+  if (device < 0 || device >= ndev) return fail_with(nullptr, CTQW_ERR_CONFIG, "invalid device index");
+  DeviceGuard g(device);
+  ctqw_ctx* h = new ctqw_ctx();
+  h->device = device;
+  h->model = md;
+  h->m = md.m;
+  h->n = md.n_sites;
+  h->dim = 1;
+  for (int p = 0; p < md.m; ++p) h->dim *= md.n_sites;
+  for (int c = 0; c < 4; ++c) {
+    // (m*eps0 + U*c), each product rounded as Python/NumPy does (hamiltonian.py:132)
+    const double a = (double)md.m * md.onsite_energy;
+    const double b = md.interaction * (double)c;
+    h->k.base[c] = a + b;
+  }
+  if (cudaMalloc((void**)&h->fail, sizeof(long long)) != cudaSuccess ||
+      cudaMalloc((void**)&h->summary_dev, sizeof(Summary)) != cudaSuccess ||
+      cudaMallocHost((void**)&h->summary_host, sizeof(Summary)) != cudaSuccess ||
+      cudaMalloc((void**)&h->small, 2 * 160 * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    ctqw_destroy(h);
+    return fail_with(nullptr, CTQW_ERR_OTHER, "cannot allocate handle buffers");
+  }
+  long long nf = kNoFail;
+  cudaMemcpy(h->fail, &nf, sizeof(nf), cudaMemcpyHostToDevice);
+  *out = h;
+  return CTQW_OK;
+}
+
+int ctqw_destroy(ctqw_handle_t h) {
+  if (!h) return CTQW_OK;
+  DeviceGuard g(h->device);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  void* dev_ptrs[] = {h->levels, h->partial, h->scl, h->stats, h->events, h->fail,
+                      h->summary_dev, h->scratch[0], h->scratch[1], h->n2_dev, h->small,
+                      h->overlap_partial};
+  for (void* p : dev_ptrs)
+    if (p) cudaFree(p);
+  if (h->summary_host) cudaFreeHost(h->summary_host);
+  delete h;
+  return CTQW_OK;
+}
+
+int ctqw_draw_noise(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64_t count,
+                    const double* levels_host, int32_t n_levels, int64_t total, double* noise_dev,
+                    void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (n_levels < 1 || !levels_host) return fail_with(h, CTQW_ERR_CONFIG, "noise level set is empty");
+  if (r0 < 0 || count < 0 || total < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative sizes");
+  for (int i = 0; i < n_levels; ++i)
+    if (!std::isfinite(levels_host[i])) return fail_with(h, CTQW_ERR_CONFIG, "noise levels must be finite");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = ensure(h, &h->levels, &h->levels_cap, n_levels, "noise levels");
+  if (rc) return rc;
+  CUDA_TRY(h, cudaMemcpyAsync(h->levels, levels_host, n_levels * sizeof(double),
+                              cudaMemcpyHostToDevice, s));
+  CUDA_TRY(h, launch_draw_noise(master_seed, r0, count, h->levels, n_levels, total, noise_dev, s));
+  // levels_host may be freed by the caller after return
+  CUDA_TRY(h, cudaStreamSynchronize(s));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
+int ctqw_build_coefficients(ctqw_handle_t h, const double* noise_dev, int64_t count,
+                            int64_t n_links, int64_t n_sites, double* hop_dev, double* site_dev,
+                            void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if ((n_links != 0 && n_links != h->n) || (n_sites != 0 && n_sites != h->n))
+    return fail_with(h, CTQW_ERR_CONFIG, "noise rows must hold 0 or N links and 0 or N sites");
+  if (n_sites && !site_dev) return fail_with(h, CTQW_ERR_CONFIG, "site_dev required for on-site noise");
+  if ((n_links || n_sites) && !noise_dev) return fail_with(h, CTQW_ERR_CONFIG, "noise_dev is NULL");
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, launch_build_coef(noise_dev, count, h->n, n_links, n_sites, h->model.tunneling,
+                                hop_dev, site_dev, (cudaStream_t)stream));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
+int ctqw_bind_coefficients(ctqw_handle_t h, int64_t count, const double* hop_dev,
+                           const double* site_dev, int64_t stride) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (!hop_dev) return fail_with(h, CTQW_ERR_CONFIG, "hop_dev is NULL");
+  if (stride != 0 && stride != h->n) return fail_with(h, CTQW_ERR_CONFIG, "stride must be 0 or N");
+  h->coef_count = count;
+  h->hop = hop_dev;
+  h->site = site_dev;
+  h->stride = stride;
+  return CTQW_OK;
+}
+
+int ctqw_fill_states(ctqw_handle_t h, double* psi_dev, int64_t count, const double* psi0_dev,
+                     void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, launch_fill_states((double2*)psi_dev, count, h->dim, (const double2*)psi0_dev,
+                                 (cudaStream_t)stream));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
+int ctqw_apply(ctqw_handle_t h, const double* psi_dev, double* out_dev, int64_t count,
+               int32_t exact, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  int rc = check_bound(h, count);
+  if (rc) return rc;
+  if (count == 0) return CTQW_OK;
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, launch_apply(h->m, (const double2*)psi_dev, (double2*)out_dev, count, h->dim, h->n,
+                           coef_of(h), h->k, exact != 0, (cudaStream_t)stream));
+  h->launches += (count + kMaxGridY - 1) / kMaxGridY;
+  return CTQW_OK;
+}
+
+int ctqw_step(ctqw_handle_t h, const double* psi_dev, double* out_dev, int64_t count,
+              const ctqw_stepper_t* stepper, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  int rc = validate_stepper(h, stepper);
+  if (rc) return rc;
+  rc = check_bound(h, count);
+  if (rc) return rc;
+  if (psi_dev == out_dev) return fail_with(h, CTQW_ERR_CONFIG, "out must not alias psi");
+  if (count == 0) return CTQW_OK;
+  DeviceGuard g(h->device);
+  rc = ensure_scratch(h, count * h->dim);
+  if (rc) return rc;
+  const StepScalars sc = scalars_for(h, stepper);
+  // Taylor: term buffers scratch[0]/[1], accumulator straight into out.
+  return generic_step(h, stepper, sc, (const double2*)psi_dev, (double2*)out_dev, h->scratch[0],
+                      (double2*)out_dev, h->scratch[1], count, nullptr, nullptr, nullptr,
+                      (cudaStream_t)stream);
+}
+
+int ctqw_check_norm(ctqw_handle_t h, double* psi_dev, int64_t count, const ctqw_stepper_t* st,
+                    double* deviations_dev, int32_t* corrected_dev, int64_t* fail_row,
+                    double* fail_deviation, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (!st) return fail_with(h, CTQW_ERR_CONFIG, "stepper is NULL");
+  if (!(0 < st->tol_norm && st->tol_norm < st->tol_fail))
+    return fail_with(h, CTQW_ERR_CONFIG, "need 0 < tol_norm < tol_fail");
+  if (count == 0) return CTQW_OK;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nparts = generic_parts(h->dim);
+  int rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
+  if (rc) return rc;
+  rc = ensure(h, &h->n2_dev, &h->n2_cap, 2 * count, "norm scratch");
+  if (rc) return rc;
+  CUDA_TRY(h, launch_norm_partial((const double2*)psi_dev, count, h->dim, h->partial, s));
+  CUDA_TRY(h, launch_norm_sum(h->partial, nparts, count, h->n2_dev, s));
+  h->launches += 2;
+  std::vector<double> n2(count), dev(count), scale(count, 1.0);
+  std::vector<int32_t> corr(count, 0);
+  CUDA_TRY(h, cudaMemcpyAsync(n2.data(), h->n2_dev, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(h, cudaStreamSynchronize(s));
+  int64_t worst = 0;
+  bool failed = false;
+  for (int64_t r = 0; r < count; ++r) {
+    dev[r] = std::fabs(n2[r] - 1.0);
+    if (dev[r] > dev[worst]) worst = r;
+    if (dev[r] > st->tol_fail) failed = true;
+  }
+  if (deviations_dev)
+    CUDA_TRY(h, cudaMemcpyAsync(deviations_dev, dev.data(), count * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+  if (failed) {
+    if (fail_row) *fail_row = worst;
+    if (fail_deviation) *fail_deviation = dev[worst];
+    if (corrected_dev) CUDA_TRY(h, cudaMemsetAsync(corrected_dev, 0, count * sizeof(int32_t), s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    char buf[160];
+    snprintf(buf, sizeof buf, "norm deviation %.3e exceeds the failure threshold (row %lld)",
+             dev[worst], (long long)worst);
+    return fail_with(h, CTQW_ERR_NUMERIC, buf);
+  }
+  bool any = false;
+  if (st->renormalize) {
+    for (int64_t r = 0; r < count; ++r)
+      if (dev[r] > st->tol_norm) {
+        corr[r] = 1;
+        scale[r] = 1.0 / std::sqrt(n2[r]);
+        any = true;
+      }
+  }
+  if (corrected_dev)
+    CUDA_TRY(h, cudaMemcpyAsync(corrected_dev, corr.data(), count * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+  if (any) {
+    CUDA_TRY(h, cudaMemcpyAsync(h->n2_dev + count, scale.data(), count * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+    CUDA_TRY(h, launch_scale_rows((double2*)psi_dev, count, h->dim, h->n2_dev + count, s));
+    h->launches += 1;
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(s));
+  return CTQW_OK;
+}
+
+int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t count,
+                int64_t first_step, int64_t n_steps, const ctqw_stepper_t* st,
+                int32_t* result_in_work, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  int rc = validate_stepper(h, st);
+  if (rc) return rc;
+  rc = check_bound(h, count);
+  if (rc) return rc;
+  if (n_steps < 0 || first_step < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative step count");
+  if (result_in_work) *result_in_work = 0;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  rc = ensure_stats(h, count);
+  if (rc) return rc;
+  h->last_count = count;
+  CUDA_TRY(h, launch_reset_stats(h->stats, h->scl, count, h->fail, s));
+  h->launches += 1;
+  if (count == 0 || n_steps == 0) return CTQW_OK;
+  const StepScalars sc = scalars_for(h, st);
+  const NormPolicy pol{st->tol_norm, st->tol_fail, st->renormalize};
+  const bool exact = st->exact != 0;
+  const Coef coef = coef_of(h);
+  double2* psi = (double2*)psi_dev;
+  double2* work = (double2*)work_dev;
+
+  if (resident_supported(h->m, h->n, sc)) {
+    timing_event(h, s);
+    CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step, n_steps,
+                                h->stats, h->events, h->fail, s));
+    timing_event(h, s);
+    h->timed_launches += h->timing ? 1 : 0;
+    h->launches += 1;
+    return CTQW_OK;
+  }
+  if (!work) return fail_with(h, CTQW_ERR_CONFIG, "work buffer required");
+  if (tile_supported(h->m, h->n, sc)) {
+    const int nparts = tile_parts(h->n, sc);
+    rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
+    if (rc) return rc;
+    double2* bufs[2] = {psi, work};
+    for (int64_t j = 0; j < n_steps; ++j) {
+      const double2* in = bufs[j & 1];
+      double2* out = bufs[(j + 1) & 1];
+      timing_event(h, s);
+      CUDA_TRY(h, launch_tile_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
+                                   h->fail, s));
+      timing_event(h, s);
+      h->timed_launches += h->timing ? 1 : 0;
+      CUDA_TRY(h, launch_norm_decide(h->partial, nparts, count, (long long)(first_step + j + 1), pol,
+                                     h->scl, h->stats, h->events, h->fail, s));
+      h->launches += 2 * ((count + kMaxGridY - 1) / kMaxGridY);
+    }
+    double2* final_buf = bufs[n_steps & 1];
+    CUDA_TRY(h, launch_rescale(final_buf, count, h->dim, h->scl, s));
+    h->launches += 2;
+    if (result_in_work) *result_in_work = (int32_t)(n_steps & 1);
+    return CTQW_OK;
+  }
+  // generic path: in place on psi; work = term buffer A, library scratch B, C
+  rc = ensure_scratch(h, count * h->dim);
+  if (rc) return rc;
+  const int nparts = generic_parts(h->dim);
+  rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
+  if (rc) return rc;
+  for (int64_t j = 0; j < n_steps; ++j) {
+    timing_event(h, s);
+    rc = generic_step(h, st, sc, psi, psi, work, h->scratch[0], h->scratch[1], count, h->scl,
+                      h->partial, h->fail, s);
+    if (rc) return rc;
+    timing_event(h, s);
+    h->timed_launches += h->timing ? 1 : 0;
+    CUDA_TRY(h, launch_norm_decide(h->partial, nparts, count, (long long)(first_step + j + 1), pol,
+                                   h->scl, h->stats, h->events, h->fail, s));
+    h->launches += 1;
+  }
+  CUDA_TRY(h, launch_rescale(psi, count, h->dim, h->scl, s));
+  h->launches += 2;
+  return CTQW_OK;
+}
+
+int ctqw_segment_stats(ctqw_handle_t h, int64_t r0, ctqw_segment_stats_t* out, void* stream) {
+  if (!h || !out) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::memset(out, 0, sizeof(*out));
+  const int64_t count = h->last_count;
+  if (count == 0) {
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    return CTQW_OK;
+  }
+  CUDA_TRY(h, launch_stats_reduce(h->stats, count, h->summary_dev, s));
+  h->launches += 1;
+  CUDA_TRY(h, cudaMemcpyAsync(h->summary_host, h->summary_dev, sizeof(Summary),
+                              cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(h, cudaStreamSynchronize(s));
+  const Summary sm = *h->summary_host;
+  out->event_count = sm.events;
+  out->corrections = sm.corrections;
+  out->max_deviation = sm.max_dev;
+  if (sm.events > 0) {
+    // First MAX_EVENTS events in (step, realization) order: each
+    // realization's own first events are stored in step order.
+    std::vector<RealStat> stats(count);
+    std::vector<EventRec> evs((size_t)count * kMaxEvents);
+    CUDA_TRY(h, cudaMemcpy(stats.data(), h->stats, count * sizeof(RealStat), cudaMemcpyDeviceToHost));
+    CUDA_TRY(h, cudaMemcpy(evs.data(), h->events, (size_t)count * kMaxEvents * sizeof(EventRec),
+                           cudaMemcpyDeviceToHost));
+    struct Item {
+      long long step;
+      int64_t r;
+      double dev;
+      int corrected;
+    };
+    std::vector<Item> items;
+    for (int64_t r = 0; r < count; ++r)
+      for (int e = 0; e < stats[r].n_ev; ++e) {
+        const EventRec& rec = evs[(size_t)r * kMaxEvents + e];
+        items.push_back(Item{rec.step_lo, r, rec.dev, rec.corrected});
+      }
+    const size_t keep = std::min<size_t>(items.size(), CTQW_MAX_EVENTS);
+    std::partial_sort(items.begin(), items.begin() + keep, items.end(),
+                      [](const Item& a, const Item& b) {
+                        return a.step != b.step ? a.step < b.step : a.r < b.r;
+                      });
+    for (size_t i = 0; i < keep; ++i) {
+      out->events[i].deviation = items[i].dev;
+      out->events[i].realization = r0 + items[i].r;
+      out->events[i].step = items[i].step;
+      out->events[i].corrected = items[i].corrected;
+    }
+    out->n_events = (int32_t)keep;
+  }
+  if (sm.fail_step != kNoFail) {
+    out->failed = 1;
+    out->fail_realization = r0 + sm.fail_row;
+    out->fail_step = sm.fail_step;
+    out->fail_deviation = sm.fail_dev;
+    char buf[200];
+    snprintf(buf, sizeof buf,
+             "norm deviation %.3e exceeds the failure threshold (realization %lld, step %lld); "
+             "reduce the time step",
+             sm.fail_dev, (long long)(r0 + sm.fail_row), (long long)sm.fail_step);
+    return fail_with(h, CTQW_ERR_NUMERIC, buf);
+  }
+  return CTQW_OK;
+}
+
+int ctqw_observe_diag(ctqw_handle_t h, const double* psi_dev, int64_t count, double* diag_sum_dev,
+                      int32_t accumulate, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, launch_observe_diag((const double2*)psi_dev, count, h->dim, diag_sum_dev,
+                                  accumulate != 0, (cudaStream_t)stream));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
+int ctqw_observe_reduce(ctqw_handle_t h, const double* diag_sum_dev, double total_count,
+                        double* populations_dev, double* scalars_dev, double* joint_dev,
+                        void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (!(total_count > 0)) return fail_with(h, CTQW_ERR_CONFIG, "total_count must be > 0");
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, launch_observe_reduce(h->m, h->n, h->dim, diag_sum_dev, total_count, populations_dev,
+                                    scalars_dev, joint_dev, h->small, (cudaStream_t)stream));
+  h->launches += populations_dev ? 3 : 2;
+  return CTQW_OK;
+}
+
+int ctqw_overlap_sumsq(ctqw_handle_t h, const double* a_dev, int64_t count_a, const double* b_dev,
+                       int64_t count_b, double* sumsq_dev, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (count_a <= 0 || count_b <= 0) return fail_with(h, CTQW_ERR_CONFIG, "empty state stack");
+  DeviceGuard g(h->device);
+  const bool same = a_dev == b_dev && count_a == count_b;
+  const int64_t parts = overlap_parts(count_a, count_b, same);
+  int rc = ensure(h, &h->overlap_partial, &h->overlap_cap, parts, "overlap partials");
+  if (rc) return rc;
+  CUDA_TRY(h, launch_overlap_sumsq((const double2*)a_dev, count_a, (const double2*)b_dev, count_b,
+                                   h->dim, h->overlap_partial, h->overlap_cap, sumsq_dev,
+                                   (cudaStream_t)stream));
+  h->launches += 2;
+  return CTQW_OK;
+}
+
+int64_t ctqw_launch_count(ctqw_handle_t h) { return h ? (int64_t)h->launches.load() : 0; }
+
+int ctqw_kernel_timing(ctqw_handle_t h, int32_t enable) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  h->timing = enable != 0;
+  h->ev_used = 0;
+  h->timed_launches = 0;
+  return CTQW_OK;
+}
+
+int ctqw_kernel_time(ctqw_handle_t h, double* total_ms, int64_t* launches, void* stream) {
+  if (!h || !total_ms || !launches) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, cudaStreamSynchronize((cudaStream_t)stream));
+  double total = 0.0;
+  for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+    float ms = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&ms, h->ev_pool[i], h->ev_pool[i + 1]));
+    total += ms;
+  }
+  *total_ms = total;
+  *launches = h->timed_launches;
+  h->ev_used = 0;
+  h->timed_launches = 0;
+  return CTQW_OK;
+}
+
+}  // extern "C"

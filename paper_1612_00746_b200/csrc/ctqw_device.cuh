@@ -1,0 +1,138 @@
+// Shared device-side definitions for libctqw (sm_100a).
+//
+// Complex128 amplitudes are double2 {re, im}.  Two arithmetic modes:
+//   EXACT = true : every product and sum rounded separately, in the order the
+//                  reference's NumPy expressions evaluate them
+//                  (hamiltonian.py:205-222, propagators.py:185-193,213-240), so
+//                  results are bit-identical to the reference between rescales.
+//   EXACT = false: the neighbour accumulations contract into DFMA (fewer FP64
+//                  instructions, one rounding per term instead of two).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ctqw {
+
+constexpr int kMaxEvents = 100;     // ensemble.py:119
+constexpr long long kNoFail = 0x7fffffffffffffffLL;
+
+// Coefficient rows of a batch: realization i reads hop + i*stride.
+struct Coef {
+  const double* hop;    // [.][N]  t + xi_link[x] for the link x -> x+1
+  const double* site;   // [.][N]  xi_site[x], nullptr when absent
+  int64_t stride;       // 0 = broadcast
+};
+
+// Norm policy, StepperConfig (propagators.py:61-86).
+struct NormPolicy {
+  double tol_norm;
+  double tol_fail;
+  int renormalize;
+};
+
+// Per-realization statistics of one evolve call (ensemble.py:459-533).
+struct RealStat {
+  long long events;
+  long long corrections;
+  long long fail_step;    // kNoFail if none
+  double max_dev;
+  double fail_dev;
+  int n_ev;               // events stored (<= kMaxEvents)
+  int pad;
+};
+
+struct EventRec {
+  double dev;
+  int step_lo;            // step number (fits 31 bits for any practical run)
+  int corrected;
+};
+
+__device__ __forceinline__ double2 cmake(double re, double im) { return make_double2(re, im); }
+
+// acc + v*z for a real coupling v (values are complex with zero imaginary
+// part in the reference; (v + 0i)*z rounds exactly like v*z component-wise).
+template <bool EXACT>
+__device__ __forceinline__ double2 madd(double2 acc, double v, double2 z) {
+  if (EXACT) {
+    acc.x = __dadd_rn(acc.x, __dmul_rn(v, z.x));
+    acc.y = __dadd_rn(acc.y, __dmul_rn(v, z.y));
+  } else {
+    acc.x = fma(v, z.x, acc.x);
+    acc.y = fma(v, z.y, acc.y);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double2 rmul(double v, double2 z) {
+  return cmake(__dmul_rn(v, z.x), __dmul_rn(v, z.y));
+}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return cmake(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+
+// z * (0 + ci i): the Taylor/RK4 coefficient -1j*dt/hbar/j has a zero real
+// part, so NumPy's complex product reduces to (-b*ci, a*ci) exactly.
+__device__ __forceinline__ double2 times_i(double ci, double2 z) {
+  return cmake(__dmul_rn(-z.y, ci), __dmul_rn(z.x, ci));
+}
+
+__device__ __forceinline__ double norm2(double2 z) { return z.x * z.x + z.y * z.y; }
+
+__device__ __forceinline__ int wrap(int x, int n) {
+  x %= n;
+  return x < 0 ? x + n : x;
+}
+
+// Block-wide sum; result valid in thread 0.  Deterministic for a fixed
+// block size (fixed shuffle tree, fixed warp order).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < nwarps; ++w) s += red[w];
+  return s;
+}
+
+// The norm policy for one realization after one step (propagators.py:316-327
+// + ensemble.py:509-533).  Returns the factor the state must be multiplied
+// by (1/sqrt(n2) when corrected -- NumPy's complex division by a real
+// multiplies by the reciprocal -- else exactly 1.0).  Sets *failed.
+__device__ __forceinline__ double norm_decide(double n2, long long step, const NormPolicy& pol,
+                                              RealStat* st, EventRec* ev, int* failed) {
+  const double dev = fabs(n2 - 1.0);
+  *failed = 0;
+  if (dev > pol.tol_fail) {
+    if (st->fail_step == kNoFail) {
+      st->fail_step = step;
+      st->fail_dev = dev;
+    }
+    *failed = 1;
+    return 1.0;
+  }
+  if (dev > st->max_dev) st->max_dev = dev;
+  if (dev > pol.tol_norm) {
+    const int corrected = pol.renormalize ? 1 : 0;
+    st->events += 1;
+    st->corrections += corrected;
+    if (st->n_ev < kMaxEvents) {
+      EventRec e;
+      e.dev = dev;
+      e.step_lo = (int)step;
+      e.corrected = corrected;
+      ev[st->n_ev] = e;
+      st->n_ev += 1;
+    }
+    if (corrected) return __ddiv_rn(1.0, __dsqrt_rn(n2));
+  }
+  return 1.0;
+}
+
+}  // namespace ctqw

@@ -1,0 +1,109 @@
+// Internal launch interface between api.cu and the kernel translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ctqw_device.cuh"
+
+namespace ctqw {
+
+constexpr int64_t kMaxGridY = 65535;
+constexpr int kMaxParts = 256;  // norm partials per realization
+
+// Diagonal base per coincidence count c: m*eps0 + U*c (hamiltonian.py:132).
+struct StencilConst {
+  double base[4];
+};
+
+// Taylor / RK4 scalars, computed on the host exactly as the reference does
+// (coeff = -1j*dt/hbar, coeff/j; propagators.py:185,191).
+struct StepScalars {
+  int backend;  // 0 taylor, 1 rk4
+  int order;    // Taylor order (applications per step); 4 for RK4
+  double ci[16];  // imaginary part of coeff/j, j = 1..order (taylor); ci[0] = coeff (rk4)
+};
+
+int generic_parts(int64_t dim);
+
+// noise.cu
+cudaError_t launch_draw_noise(uint64_t master_seed, int64_t r0, int64_t count,
+                              const double* levels_dev, int n_levels, int64_t total,
+                              double* out, cudaStream_t s);
+cudaError_t launch_build_coef(const double* noise, int64_t count, int n, int64_t n_links,
+                              int64_t n_sites, double t, double* hop, double* site,
+                              cudaStream_t s);
+cudaError_t launch_fill_states(double2* psi, int64_t count, int64_t dim, const double2* psi0,
+                               cudaStream_t s);
+
+// stencil_generic.cu
+cudaError_t launch_apply(int m, const double2* psi, double2* out, int64_t count, int64_t dim,
+                         int n, const Coef& coef, const StencilConst& k, bool exact,
+                         cudaStream_t s);
+cudaError_t launch_taylor_order(int m, bool exact, bool scale, const double2* term_in,
+                                double2* term_out, const double2* acc_in, double2* acc_out,
+                                int64_t count, int64_t dim, int n, const Coef& coef,
+                                const StencilConst& k, double ci, const double* scl,
+                                double* partial, const long long* fail, cudaStream_t s);
+cudaError_t launch_rk4_stage(int m, bool exact, bool scale, int stage, const double2* arg_in,
+                             const double2* psi, const double2* out_in, double2* arg_out,
+                             double2* out_out, int64_t count, int64_t dim, int n,
+                             const Coef& coef, const StencilConst& k, double ci,
+                             const double* scl, double* partial, const long long* fail,
+                             cudaStream_t s);
+cudaError_t launch_norm_partial(const double2* psi, int64_t count, int64_t dim, double* partial,
+                                cudaStream_t s);
+
+// step_tile.cu (m = 2 fused paths)
+struct TileGeom {
+  int n;       // ring length
+  int nt;      // tiles per axis
+  int halo;    // stencil applications per step
+};
+bool tile_supported(int m, int n, const StepScalars& sc);
+bool resident_supported(int m, int n, const StepScalars& sc);
+int tile_parts(int n, const StepScalars& sc);
+cudaError_t launch_tile_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
+                             const Coef& coef, const StencilConst& k, const StepScalars& sc,
+                             bool exact, const double* scl, double* partial,
+                             const long long* fail, cudaStream_t s);
+cudaError_t launch_resident(double2* psi, int64_t count, int n, const Coef& coef,
+                            const StencilConst& k, const StepScalars& sc, bool exact,
+                            const NormPolicy& pol, long long first_step, long long n_steps,
+                            RealStat* stats, EventRec* events, long long* fail,
+                            cudaStream_t s);
+
+// norm_observe.cu
+cudaError_t launch_norm_decide(const double* partial, int nparts, int64_t count,
+                               long long step, const NormPolicy& pol, double* scl,
+                               RealStat* stats, EventRec* events, long long* fail,
+                               cudaStream_t s);
+cudaError_t launch_rescale(double2* psi, int64_t count, int64_t dim, double* scl,
+                           cudaStream_t s);
+cudaError_t launch_reset_stats(RealStat* stats, double* scl, int64_t count, long long* fail,
+                               cudaStream_t s);
+struct Summary {
+  long long events;
+  long long corrections;
+  double max_dev;
+  long long fail_step;
+  long long fail_row;
+  double fail_dev;
+};
+cudaError_t launch_stats_reduce(const RealStat* stats, int64_t count, Summary* out,
+                                cudaStream_t s);
+cudaError_t launch_norm_sum(const double* partial, int nparts, int64_t count, double* n2,
+                            cudaStream_t s);
+cudaError_t launch_scale_rows(double2* psi, int64_t count, int64_t dim, const double* scl,
+                              cudaStream_t s);
+cudaError_t launch_observe_diag(const double2* psi, int64_t count, int64_t dim, double* diag,
+                                bool accumulate, cudaStream_t s);
+cudaError_t launch_observe_reduce(int m, int n, int64_t dim, const double* diag_sum,
+                                  double total, double* pops, double* scalars, double* joint,
+                                  double* scratch, cudaStream_t s);
+cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b, int64_t rb,
+                                 int64_t dim, double* partial, int64_t nparts_cap,
+                                 double* out, cudaStream_t s);
+int64_t overlap_parts(int64_t ra, int64_t rb, bool same);
+
+}  // namespace ctqw

@@ -1,0 +1,359 @@
+// Norm policy bookkeeping and ensemble observables.
+//
+// Norm policy (propagators.py:309-328, ensemble.py:509-533): the step kernels
+// leave per-realization |psi|^2 partials; norm_decide_kernel sums them in a
+// fixed order, records deviation statistics/events and the rescale factor,
+// which the NEXT step's kernel applies while loading (the step is linear, so a
+// lazy rescale is exact).  rescale_kernel applies the last step's factor at
+// the end of a segment.
+//
+// Observables: only diag(rho) = mean_r |psi_r|^2 is needed for populations,
+// position moments, participation ratio and the joint distribution
+// (observables.py:34-101); purity needs the realization overlaps
+// sum_{r,s} |<psi_r|psi_s>|^2 instead of the dense D x D Gram
+// (density.py:91-92).
+#include "ctqw_device.cuh"
+#include "kernels.h"
+
+namespace ctqw {
+
+namespace {
+
+__global__ void norm_decide_kernel(const double* __restrict__ partial, int nparts, int64_t count,
+                                   long long step, NormPolicy pol, double* scl, RealStat* stats,
+                                   EventRec* events, long long* fail) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= count) return;
+  if (*fail < step) return;  // an earlier step already failed: run is over
+  double n2 = 0.0;
+  const double* p = partial + r * nparts;
+  for (int i = 0; i < nparts; ++i) n2 += p[i];
+  int failed = 0;
+  scl[r] = norm_decide(n2, step, pol, stats + r, events + r * kMaxEvents, &failed);
+  if (failed) atomicMin(reinterpret_cast<unsigned long long*>(fail), (unsigned long long)step);
+}
+
+__global__ void rescale_kernel(double2* psi, int64_t dim, double* scl) {
+  const int64_t r = blockIdx.y;
+  const double s = scl[r];
+  if (s == 1.0) return;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < dim;
+       a += (int64_t)gridDim.x * blockDim.x)
+    psi[r * dim + a] = rmul(s, psi[r * dim + a]);
+}
+
+__global__ void reset_scale_kernel(double* scl, int64_t count) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < count) scl[r] = 1.0;
+}
+
+__global__ void reset_stats_kernel(RealStat* stats, double* scl, int64_t count, long long* fail) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) *fail = kNoFail;
+  if (r >= count) return;
+  RealStat z;
+  z.events = 0;
+  z.corrections = 0;
+  z.fail_step = kNoFail;
+  z.max_dev = 0.0;
+  z.fail_dev = 0.0;
+  z.n_ev = 0;
+  z.pad = 0;
+  stats[r] = z;
+  scl[r] = 1.0;
+}
+
+// Totals over realizations; the failure is the earliest failing step, and at
+// that step the largest deviation (np.argmax picks the lowest row on ties).
+__global__ void stats_reduce_kernel(const RealStat* __restrict__ stats, int64_t count,
+                                    Summary* out) {
+  __shared__ long long s_ev[1024], s_cor[1024], s_fs[1024], s_fr[1024];
+  __shared__ double s_md[1024], s_fd[1024];
+  const int tid = threadIdx.x;
+  long long ev = 0, cor = 0, fs = kNoFail, fr = -1;
+  double md = 0.0, fd = 0.0;
+  for (int64_t r = tid; r < count; r += blockDim.x) {
+    const RealStat st = stats[r];
+    ev += st.events;
+    cor += st.corrections;
+    if (st.max_dev > md) md = st.max_dev;
+    if (st.fail_step != kNoFail) {
+      if (st.fail_step < fs || (st.fail_step == fs && (st.fail_dev > fd || (st.fail_dev == fd && r < fr)))) {
+        fs = st.fail_step;
+        fd = st.fail_dev;
+        fr = r;
+      }
+    }
+  }
+  s_ev[tid] = ev;
+  s_cor[tid] = cor;
+  s_md[tid] = md;
+  s_fs[tid] = fs;
+  s_fd[tid] = fd;
+  s_fr[tid] = fr;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (tid < o) {
+      s_ev[tid] += s_ev[tid + o];
+      s_cor[tid] += s_cor[tid + o];
+      if (s_md[tid + o] > s_md[tid]) s_md[tid] = s_md[tid + o];
+      const long long fs2 = s_fs[tid + o];
+      const double fd2 = s_fd[tid + o];
+      const long long fr2 = s_fr[tid + o];
+      if (fs2 != kNoFail &&
+          (fs2 < s_fs[tid] || (fs2 == s_fs[tid] && (fd2 > s_fd[tid] || (fd2 == s_fd[tid] && fr2 < s_fr[tid]))))) {
+        s_fs[tid] = fs2;
+        s_fd[tid] = fd2;
+        s_fr[tid] = fr2;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    Summary sm;
+    sm.events = s_ev[0];
+    sm.corrections = s_cor[0];
+    sm.max_dev = s_md[0];
+    sm.fail_step = s_fs[0];
+    sm.fail_row = s_fr[0];
+    sm.fail_dev = s_fd[0];
+    *out = sm;
+  }
+}
+
+__global__ void norm_sum_kernel(const double* __restrict__ partial, int nparts, int64_t count,
+                                double* n2) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= count) return;
+  double s = 0.0;
+  for (int i = 0; i < nparts; ++i) s += partial[r * nparts + i];
+  n2[r] = s;
+}
+
+// diag[alpha] (+)= sum_r |psi_r(alpha)|^2 in realization order.
+__global__ void observe_diag_kernel(const double2* __restrict__ psi, int64_t count, int64_t dim,
+                                    double* diag, int accumulate) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= dim) return;
+  double s = accumulate ? diag[a] : 0.0;
+  int64_t r = 0;
+  for (; r + 4 <= count; r += 4) {
+    const double2 v0 = __ldg(psi + (r + 0) * dim + a);
+    const double2 v1 = __ldg(psi + (r + 1) * dim + a);
+    const double2 v2 = __ldg(psi + (r + 2) * dim + a);
+    const double2 v3 = __ldg(psi + (r + 3) * dim + a);
+    s += norm2(v0);
+    s += norm2(v1);
+    s += norm2(v2);
+    s += norm2(v3);
+  }
+  for (; r < count; ++r) s += norm2(__ldg(psi + r * dim + a));
+  diag[a] = s;
+}
+
+// populations[x] = sum_p sum_{alpha: x_p = x} p(alpha), p = diag/total.
+__global__ void populations_kernel(int m, int n, const double* __restrict__ diag, double total,
+                                   double* pops) {
+  __shared__ double red[32];
+  const int x = blockIdx.x;
+  const int64_t plane = m == 1 ? 1 : (m == 2 ? (int64_t)n : (int64_t)n * n);
+  double acc = 0.0;
+  for (int p = 0; p < m; ++p) {
+    // joint states with digit p equal to x: enumerate the other m-1 digits
+    int64_t stride_p = 1;
+    for (int q = p + 1; q < m; ++q) stride_p *= n;
+    for (int64_t j = threadIdx.x; j < plane; j += blockDim.x) {
+      // j enumerates the remaining digits; split into high (above p) and low parts
+      const int64_t low = j % stride_p;
+      const int64_t high = j / stride_p;
+      const int64_t alpha = (high * n + x) * stride_p + low;
+      acc += diag[alpha] / total;
+    }
+  }
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) pops[x] = b;
+}
+
+__global__ void joint_sums_kernel(const double* __restrict__ diag, int64_t dim, double total,
+                                  double* partial, double* joint) {
+  __shared__ double red[32];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < dim;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const double p = diag[a] / total;
+    if (joint) joint[a] = p;
+    s1 += p;
+    s2 += p * p;
+  }
+  const double b1 = block_sum(s1, red);
+  const double b2 = block_sum(s2, red);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = b1;
+    partial[2 * blockIdx.x + 1] = b2;
+  }
+}
+
+__global__ void joint_final_kernel(const double* __restrict__ partial, int nparts,
+                                   double* scalars) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s1 = 0.0, s2 = 0.0;
+  for (int i = 0; i < nparts; ++i) {
+    s1 += partial[2 * i];
+    s2 += partial[2 * i + 1];
+  }
+  scalars[0] = s1;
+  scalars[1] = s2;
+  // participation ratio 1 / sum (p/S1)^2 = S1^2 / S2  (observables.py:94-101)
+  scalars[2] = s2 > 0.0 ? (s1 * s1) / s2 : 0.0;
+}
+
+// sum_{i,j} |<a_i|b_j>|^2 : 32 x 32 blocks of the overlap matrix, each
+// thread a 2 x 2 sub-block, D swept in chunks staged through shared memory.
+constexpr int kOT = 32;   // overlap tile
+constexpr int kOK = 16;   // D chunk
+
+__global__ void __launch_bounds__(256) overlap_kernel(const double2* __restrict__ a, int64_t ra,
+                                                      const double2* __restrict__ b, int64_t rb,
+                                                      int64_t dim, int same, int64_t ntj,
+                                                      double* partial) {
+  __shared__ double2 sa[kOK][kOT + 1];
+  __shared__ double2 sb[kOK][kOT + 1];
+  __shared__ double red[32];
+  const int64_t ti = blockIdx.x / ntj, tj = blockIdx.x % ntj;
+  const int tid = threadIdx.x;
+  if (same && tj < ti) {
+    if (tid == 0) partial[blockIdx.x] = 0.0;
+    return;
+  }
+  const int li = (tid / 16) * 2, lj = (tid % 16) * 2;
+  double2 g[2][2];
+  for (int u = 0; u < 2; ++u)
+    for (int v = 0; v < 2; ++v) g[u][v] = make_double2(0.0, 0.0);
+  for (int64_t k0 = 0; k0 < dim; k0 += kOK) {
+    for (int e = tid; e < kOK * kOT; e += 256) {
+      const int kk = e % kOK, rr = e / kOK;
+      const int64_t gi = ti * kOT + rr, gj = tj * kOT + rr, gk = k0 + kk;
+      sa[kk][rr] = (gi < ra && gk < dim) ? a[gi * dim + gk] : make_double2(0.0, 0.0);
+      sb[kk][rr] = (gj < rb && gk < dim) ? b[gj * dim + gk] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kOK; ++kk) {
+      double2 av[2], bv[2];
+      for (int u = 0; u < 2; ++u) av[u] = sa[kk][li + u];
+      for (int v = 0; v < 2; ++v) bv[v] = sb[kk][lj + v];
+      for (int u = 0; u < 2; ++u)
+        for (int v = 0; v < 2; ++v) {
+          // conj(a) * b
+          g[u][v].x = fma(av[u].x, bv[v].x, fma(av[u].y, bv[v].y, g[u][v].x));
+          g[u][v].y = fma(av[u].x, bv[v].y, fma(-av[u].y, bv[v].x, g[u][v].y));
+        }
+    }
+    __syncthreads();
+  }
+  double s = 0.0;
+  for (int u = 0; u < 2; ++u)
+    for (int v = 0; v < 2; ++v) s += norm2(g[u][v]);
+  const double tot = block_sum(s, red);
+  if (tid == 0) partial[blockIdx.x] = (same && tj > ti) ? 2.0 * tot : tot;
+}
+
+__global__ void sum_kernel(const double* __restrict__ partial, int64_t nparts, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < nparts; i += blockDim.x) s += partial[i];
+  const double b = block_sum(s, red);
+  if (threadIdx.x == 0) out[0] = b;
+}
+
+}  // namespace
+
+cudaError_t launch_norm_decide(const double* partial, int nparts, int64_t count, long long step,
+                               const NormPolicy& pol, double* scl, RealStat* stats,
+                               EventRec* events, long long* fail, cudaStream_t s) {
+  const int bs = 128;
+  norm_decide_kernel<<<(unsigned)((count + bs - 1) / bs), bs, 0, s>>>(partial, nparts, count, step,
+                                                                       pol, scl, stats, events, fail);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rescale(double2* psi, int64_t count, int64_t dim, double* scl, cudaStream_t s) {
+  const int bs = 256;
+  int64_t blocks = (dim + bs - 1) / bs;
+  if (blocks > 64) blocks = 64;
+  for (int64_t r0 = 0; r0 < count; r0 += kMaxGridY) {
+    const int64_t rows = count - r0 < kMaxGridY ? count - r0 : kMaxGridY;
+    rescale_kernel<<<dim3((unsigned)blocks, (unsigned)rows), bs, 0, s>>>(psi + r0 * dim, dim, scl + r0);
+  }
+  reset_scale_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(scl, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_rows(double2* psi, int64_t count, int64_t dim, const double* scl,
+                              cudaStream_t s) {
+  const int bs = 256;
+  int64_t blocks = (dim + bs - 1) / bs;
+  if (blocks > 64) blocks = 64;
+  for (int64_t r0 = 0; r0 < count; r0 += kMaxGridY) {
+    const int64_t rows = count - r0 < kMaxGridY ? count - r0 : kMaxGridY;
+    rescale_kernel<<<dim3((unsigned)blocks, (unsigned)rows), bs, 0, s>>>(psi + r0 * dim, dim,
+                                                                         const_cast<double*>(scl) + r0);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset_stats(RealStat* stats, double* scl, int64_t count, long long* fail,
+                               cudaStream_t s) {
+  const int64_t work = count > 0 ? count : 1;
+  reset_stats_kernel<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(stats, scl, count, fail);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_reduce(const RealStat* stats, int64_t count, Summary* out, cudaStream_t s) {
+  stats_reduce_kernel<<<1, 1024, 0, s>>>(stats, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm_sum(const double* partial, int nparts, int64_t count, double* n2,
+                            cudaStream_t s) {
+  norm_sum_kernel<<<(unsigned)((count + 127) / 128), 128, 0, s>>>(partial, nparts, count, n2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_observe_diag(const double2* psi, int64_t count, int64_t dim, double* diag,
+                                bool accumulate, cudaStream_t s) {
+  const int bs = 256;
+  observe_diag_kernel<<<(unsigned)((dim + bs - 1) / bs), bs, 0, s>>>(psi, count, dim, diag,
+                                                                      accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_observe_reduce(int m, int n, int64_t dim, const double* diag_sum, double total,
+                                  double* pops, double* scalars, double* joint, double* scratch,
+                                  cudaStream_t s) {
+  if (pops) populations_kernel<<<n, 256, 0, s>>>(m, n, diag_sum, total, pops);
+  const int nparts = 148;
+  joint_sums_kernel<<<nparts, 256, 0, s>>>(diag_sum, dim, total, scratch, joint);
+  joint_final_kernel<<<1, 32, 0, s>>>(scratch, nparts, scalars);
+  return cudaGetLastError();
+}
+
+int64_t overlap_parts(int64_t ra, int64_t rb, bool same) {
+  (void)same;
+  const int64_t ti = (ra + kOT - 1) / kOT, tj = (rb + kOT - 1) / kOT;
+  return ti * tj;
+}
+
+cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b, int64_t rb,
+                                 int64_t dim, double* partial, int64_t nparts_cap, double* out,
+                                 cudaStream_t s) {
+  const bool same = (a == b) && (ra == rb);
+  const int64_t ntj = (rb + kOT - 1) / kOT;
+  const int64_t nparts = overlap_parts(ra, rb, same);
+  if (nparts > nparts_cap) return cudaErrorInvalidValue;
+  overlap_kernel<<<(unsigned)nparts, 256, 0, s>>>(a, ra, b, rb, dim, same ? 1 : 0, ntj, partial);
+  sum_kernel<<<1, 1024, 0, s>>>(partial, nparts, out);
+  return cudaGetLastError();
+}
+
+}  // namespace ctqw

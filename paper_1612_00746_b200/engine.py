@@ -1,0 +1,530 @@
+"""Ensemble run: the drop-in replacement of ``ctqw.ensemble.run`` for static noise.
+
+Keeps the reference's configuration and output API -- ``RunConfig``,
+``InitialStateSpec``, ``build_initial_state``, ``OutputSinks`` /
+``MemorySinks``, ``RunReport``, ``estimate_memory``, ``run(config, sinks)``
+(ensemble.py:122-804) -- and replaces its engine:
+
+* the realization stack lives in HBM for the whole run (one contiguous shard
+  per GPU when torch.distributed is initialised, see ``sharding``);
+* the noise draw and the stencil coefficients are generated on the device;
+* each segment between collection points is one ``ctqw_evolve`` call (the
+  reference's ``_evolve_segment``, ensemble.py:445-558) -- fused step kernels
+  with the per-step norm policy on the device;
+* at each collection point the diagonal of the ensemble-averaged density
+  matrix is summed on the device, all-reduced across GPUs, and reduced to
+  the observable rows in the reference's row order (ensemble.py:609-632).
+
+Results match the reference's ``run(..., precision="double")`` to rounding
+(1e-10 relative is the acceptance bar; bit-identical between renormalisation
+events in ``exact`` mode).
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import sharding
+from .errors import CapacityError, ConfigurationError, MemoryBudgetError, NormFailureError
+from .geometry import JointSpace, build_topology, joint_index
+from .hamiltonian import CouplingModel, handle_for
+from .noise import NoiseSpec, draw_noise
+from .observables import DiagonalDensity, position_stats_from_populations
+from .profiling import (
+    STAGE_DENSITY,
+    STAGE_EVOLUTION,
+    STAGE_HAMILTONIAN,
+    STAGE_INITIALIZATION,
+    StageProfile,
+)
+from .propagators import BACKEND_EIGEN, NormEvent, StepperConfig
+
+PRECISION_SINGLE = "single"
+PRECISION_DOUBLE = "double"
+PRECISIONS = (PRECISION_SINGLE, PRECISION_DOUBLE)
+
+KIND_AUTO = "auto"
+KIND_SINGLE_SITE = "single_site"
+KIND_PRODUCT = "product"
+KIND_SYMMETRIZED = "symmetrized_pair"
+KIND_ANTISYMMETRIZED = "antisymmetrized_pair"
+KIND_CUSTOM = "custom_vector"
+STATE_KINDS = (KIND_AUTO, KIND_SINGLE_SITE, KIND_PRODUCT, KIND_SYMMETRIZED,
+               KIND_ANTISYMMETRIZED, KIND_CUSTOM)
+
+OBS_POPULATIONS = "populations"
+OBS_POSITION = "position_mean_variance"
+OBS_PURITY = "purity"
+OBS_PARTICIPATION = "participation_ratio"
+OBS_JOINT = "joint_distribution"
+KNOWN_OBSERVABLES = (OBS_POPULATIONS, OBS_POSITION, OBS_PURITY, OBS_PARTICIPATION, OBS_JOINT)
+
+WORKERS_ENV = "CTQW_WORKERS"
+MAX_EVENTS_PER_SEGMENT = 100
+# sum_{r,s} |<psi_r|psi_s>|^2 costs R^2 * D complex multiply-adds per snapshot
+PURITY_WORK_CAP = 2**40
+PURITY_GATHER_CAP = 2 * 2**30
+
+
+@dataclass(frozen=True)
+class InitialStateSpec:
+    kind: str = KIND_AUTO
+    positions: tuple | None = None
+    amplitudes: np.ndarray | None = None
+
+    def __post_init__(self):
+        if self.kind not in STATE_KINDS:
+            raise ConfigurationError(f"initial state kind {self.kind!r} not recognized; use one of {STATE_KINDS}")
+        if self.positions is not None:
+            object.__setattr__(self, "positions", tuple(int(x) for x in self.positions))
+
+
+def build_initial_state(spec: InitialStateSpec, space: JointSpace) -> np.ndarray:
+    """Unit-norm joint state (ensemble.py:147-216), complex128 on the host."""
+    n, m = space.lattice.n_sites, space.m
+    kind = spec.kind
+    if kind == KIND_AUTO:
+        kind = KIND_SINGLE_SITE if m == 1 else KIND_PRODUCT
+    if kind == KIND_CUSTOM:
+        if spec.amplitudes is None:
+            raise ConfigurationError("custom_vector needs explicit amplitudes")
+        amps = np.asarray(spec.amplitudes, dtype=np.complex128)
+        if amps.shape != (space.dim,):
+            raise ConfigurationError(f"custom vector has shape {amps.shape}, expected ({space.dim},)")
+        norm = np.linalg.norm(amps)
+        if norm == 0:
+            raise ConfigurationError("custom vector has zero norm")
+        return amps / norm
+    psi = np.zeros(space.dim, dtype=np.complex128)
+    if kind == KIND_SINGLE_SITE:
+        if m != 1:
+            raise ConfigurationError("single_site describes one particle only")
+        pos = spec.positions if spec.positions is not None else ((n - 1) // 2,)
+        if len(pos) != 1:
+            raise ConfigurationError("single_site takes exactly one position")
+        psi[joint_index(pos, space)] = 1.0
+        return psi
+    if kind == KIND_PRODUCT:
+        pos = spec.positions
+        if pos is None:
+            if m > n:
+                raise ConfigurationError(f"no default product placement for {m} particles on {n} sites")
+            first = (n - m) // 2
+            pos = tuple(range(first, first + m))
+        if len(pos) != m:
+            raise ConfigurationError(f"product state needs {m} positions, got {len(pos)}")
+        psi[joint_index(pos, space)] = 1.0
+        return psi
+    if m != 2:
+        raise ConfigurationError(f"{kind} requires exactly two particles")
+    pos = spec.positions
+    if pos is None:
+        first = (n - 2) // 2
+        pos = (first, first + 1)
+    if len(pos) != 2:
+        raise ConfigurationError(f"{kind} takes exactly two positions")
+    x, y = pos
+    if x == y:
+        if kind == KIND_ANTISYMMETRIZED:
+            raise ConfigurationError("antisymmetrized pair on one site vanishes identically")
+        psi[joint_index((x, x), space)] = 1.0
+        return psi
+    amp = 1.0 / np.sqrt(2.0)
+    psi[joint_index((x, y), space)] = amp
+    psi[joint_index((y, x), space)] = (-1.0 if kind == KIND_ANTISYMMETRIZED else 1.0) * amp
+    return psi
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    """The reference's run description (ensemble.py:219-294) plus two B200 knobs.
+
+    ``exact``: reference operation order without FMA (bit-identical between
+    renormalisations) vs FMA-contracted stencil.  ``device``: CUDA device
+    index (default: the current device / LOCAL_RANK).
+    """
+
+    space: JointSpace
+    model: CouplingModel = CouplingModel()
+    noise: NoiseSpec = NoiseSpec()
+    stepper: StepperConfig = StepperConfig()
+    initial: InitialStateSpec = InitialStateSpec()
+    realizations: int = 1000
+    steps: int = 1500
+    post_rate: int = 10
+    master_seed: int = 1234
+    workers: int = 0
+    precision: str = PRECISION_SINGLE
+    observables: tuple | None = None
+    memory_budget: int = 4 * 2**30
+    dense_cap: int = 4096
+    exact: bool = True
+    device: int | None = None
+
+    def __post_init__(self):
+        if self.realizations < 1:
+            raise ConfigurationError(f"realizations = {self.realizations} must be >= 1")
+        if self.steps < 0:
+            raise ConfigurationError(f"steps = {self.steps} must be >= 0")
+        if self.post_rate < 1:
+            raise ConfigurationError(f"post_rate = {self.post_rate} must be >= 1")
+        if self.steps > 0 and self.post_rate > self.steps:
+            raise ConfigurationError(f"post_rate = {self.post_rate} exceeds steps = {self.steps}")
+        if self.workers < 0:
+            raise ConfigurationError(f"workers = {self.workers} must be >= 0")
+        if self.precision not in PRECISIONS:
+            raise ConfigurationError(f"precision {self.precision!r} not recognized; use one of {PRECISIONS}")
+        if self.memory_budget <= 0:
+            raise ConfigurationError("memory_budget must be positive")
+        if self.observables is None:
+            names = [OBS_POPULATIONS, OBS_PURITY, OBS_PARTICIPATION]
+            if self.space.lattice.q == 1:
+                names.insert(1, OBS_POSITION)
+            object.__setattr__(self, "observables", tuple(names))
+        else:
+            object.__setattr__(self, "observables", tuple(self.observables))
+            for name in self.observables:
+                if name not in KNOWN_OBSERVABLES:
+                    raise ConfigurationError(f"observable {name!r} not recognized; use one of {KNOWN_OBSERVABLES}")
+            if not self.observables:
+                raise ConfigurationError("observable selection is empty")
+        if OBS_POSITION in self.observables and self.space.lattice.q != 1:
+            raise ConfigurationError("position_mean_variance is only defined on one-direction lattices")
+
+    @property
+    def dtype(self):
+        return np.complex128
+
+    @property
+    def schedule(self) -> tuple:
+        if self.steps == 0:
+            return (0,)
+        pts = list(range(self.post_rate, self.steps + 1, self.post_rate))
+        if pts[-1] != self.steps:
+            pts.append(self.steps)
+        return tuple(pts)
+
+
+def estimate_memory(config: RunConfig, world: int = 1) -> dict:
+    """Device working set per GPU in bytes (keys of ensemble.py:297-323).
+
+    States are complex128 regardless of ``precision``; the stack and one
+    work buffer of the same size (ping-pong of the streaming path), O(N)
+    coefficients per realization instead of the (D, H+1) value table, no
+    topology table, and the D-double diagonal instead of the packed rho.
+    """
+    space = config.space
+    dim = space.dim
+    n = space.lattice.n_sites
+    r_local = -(-config.realizations // world)
+    state = r_local * dim * 16
+    coeff = r_local * n * 8 * 3
+    return {
+        "joint_dim": dim,
+        "itemsize": 16,
+        "state_bytes": 2 * state,
+        "hamiltonian_bytes": coeff,
+        "topology_bytes": 0,
+        "density_bytes": dim * 8 * 2,
+        "total_bytes": 2 * state + coeff + dim * 16,
+    }
+
+
+class OutputSinks:
+    def observable_rows(self, time_tag: float, rows):
+        pass
+
+    def density_snapshot(self, rho, step: int):
+        pass
+
+    def norm_events(self, events):
+        pass
+
+    def message(self, text: str):
+        pass
+
+    def finish(self, report):
+        pass
+
+
+class MemorySinks(OutputSinks):
+    def __init__(self, keep_densities: bool = True, max_events: int = 1000):
+        self.keep_densities = keep_densities
+        self.max_events = max_events
+        self.rows = []
+        self.densities = []
+        self.events = []
+        self.messages = []
+        self.report = None
+
+    def observable_rows(self, time_tag, rows):
+        self.rows.extend((time_tag, name, idx, value) for name, idx, value in rows)
+
+    def density_snapshot(self, rho, step):
+        if self.keep_densities:
+            self.densities.append(rho)
+
+    def norm_events(self, events):
+        room = self.max_events - len(self.events)
+        if room > 0:
+            self.events.extend(events[:room])
+
+    def message(self, text):
+        self.messages.append(text)
+
+    def finish(self, report):
+        self.report = report
+
+
+@dataclass
+class RunReport:
+    config: RunConfig
+    profile: StageProfile
+    io_seconds: float
+    wall_seconds: float
+    workers: int
+    snapshots: int
+    max_norm_deviation: float
+    norm_corrections: int
+    norm_events: int
+    switch_count: int
+    memory_estimate: dict
+
+
+def _default_device():
+    import torch
+
+    if not torch.cuda.is_available():
+        from .errors import NativeError
+
+        raise NativeError("no CUDA device: the B200 path has no CPU fallback")
+    env = os.environ.get("LOCAL_RANK")
+    if env is not None and torch.distributed.is_initialized():
+        return int(env) % torch.cuda.device_count()
+    return torch.cuda.current_device()
+
+
+class EnsembleState:
+    """Device-resident shard of one run: noise, coefficients, states.
+
+    Exposed so benchmarks and tests can drive segments directly; ``run``
+    is the public entry point.
+    """
+
+    def __init__(self, config: RunConfig, device: int, lo: int, hi: int):
+        import torch
+
+        self.config = config
+        self.lo, self.hi = lo, hi
+        self.count = hi - lo
+        space = config.space
+        self.topology = build_topology(space)
+        model = config.model
+        self.handle = handle_for(space.m, space.lattice.n_sites, model.onsite_energy,
+                                 model.ring_tunneling(), model.interaction, model.hbar, device)
+        self.dev = torch.device(f"cuda:{device}")
+        n = space.lattice.n_sites
+        noise, n_links, n_sites = draw_noise(self.handle, config.noise, config.master_seed, lo,
+                                             self.count)
+        self.hop = torch.empty((max(self.count, 1), n), dtype=torch.float64, device=self.dev)
+        self.site = (torch.empty((max(self.count, 1), n), dtype=torch.float64, device=self.dev)
+                     if n_sites else None)
+        if self.count:
+            self.handle.build_coefficients(noise.contiguous(), self.count, n_links, n_sites,
+                                           self.hop, self.site)
+        self.handle.bind(self.hop, self.site, self.count, n)
+        del noise
+        psi0 = build_initial_state(config.initial, space)
+        self.psi0 = torch.as_tensor(psi0, device=self.dev)
+        self.psi = torch.empty((max(self.count, 1), space.dim), dtype=torch.complex128, device=self.dev)
+        self.work = torch.empty_like(self.psi)
+        if self.count:
+            self.handle.fill_states(self.psi, self.count, self.psi0)
+        self.stepper = config.stepper.native(config.exact)
+
+    def evolve(self, first_step: int, n_steps: int):
+        """Enqueue ``n_steps`` steps (asynchronous)."""
+        if self.count == 0 or n_steps == 0:
+            self.handle.evolve(self.psi, self.work, 0, first_step, 0, self.stepper)
+            return
+        swapped = self.handle.evolve(self.psi, self.work, self.count, first_step, n_steps,
+                                     self.stepper)
+        if swapped:
+            self.psi, self.work = self.work, self.psi
+
+    def stats(self) -> dict:
+        st = self.handle.segment_stats(self.lo)
+        events = [(e.deviation, bool(e.corrected), int(e.realization), int(e.step))
+                  for e in st.events[: st.n_events]]
+        failure = None
+        if st.failed:
+            failure = (float(st.fail_deviation), int(st.fail_realization), int(st.fail_step))
+        return {"event_count": int(st.event_count), "corrections": int(st.corrections),
+                "max_deviation": float(st.max_deviation), "events": events, "failure": failure}
+
+    def diagonal_sum(self, out):
+        self.handle.observe_diag(self.psi, self.count, out, accumulate=False)
+        return out
+
+    def states(self):
+        return self.psi[: self.count]
+
+
+def _observable_rows(config, pops, pr, purity, joint):
+    rows = []
+    for name in config.observables:
+        if name == OBS_POPULATIONS:
+            rows.extend(("population", i, float(v)) for i, v in enumerate(pops))
+        elif name == OBS_POSITION:
+            st = position_stats_from_populations(pops, config.space.lattice.boundary == "periodic")
+            rows.append(("position_mean", 0, st.mean))
+            rows.append(("position_variance", 0, st.variance))
+            rows.append(("position_wrapped", 0, float(st.wrapped)))
+        elif name == OBS_PURITY:
+            rows.append(("purity", 0, purity))
+        elif name == OBS_PARTICIPATION:
+            rows.append(("participation_ratio", 0, pr))
+        elif name == OBS_JOINT:
+            rows.extend(("joint_probability", i, float(v)) for i, v in enumerate(joint))
+    return rows
+
+
+def collect_observables(config, ens: EnsembleState, group=None, want_joint=None):
+    """Device reduction of one collection point -> (pops, pr, purity, joint, diag)."""
+    import torch
+
+    space = config.space
+    dim = space.dim
+    n = space.lattice.n_sites
+    diag = torch.empty(dim, dtype=torch.float64, device=ens.dev)
+    if ens.count:
+        ens.diagonal_sum(diag)
+    else:
+        diag.zero_()
+    sharding.allreduce_sum_(diag, group)
+    pops = torch.empty(n, dtype=torch.float64, device=ens.dev)
+    scalars = torch.empty(3, dtype=torch.float64, device=ens.dev)
+    need_joint = OBS_JOINT in config.observables if want_joint is None else want_joint
+    joint = torch.empty(dim, dtype=torch.float64, device=ens.dev) if need_joint else None
+    ens.handle.observe_reduce(diag, float(config.realizations), pops, scalars, joint)
+    purity = None
+    if OBS_PURITY in config.observables:
+        states = sharding.gather_states(ens.states(), group)
+        out = torch.empty(1, dtype=torch.float64, device=ens.dev)
+        ens.handle.overlap_sumsq(states, states.shape[0], states, states.shape[0], out)
+        purity = float(out.item()) / float(config.realizations) ** 2
+    pops_h = pops.cpu().numpy()
+    sc = scalars.cpu().numpy()
+    joint_h = joint.cpu().numpy() if joint is not None else None
+    return pops_h, float(sc[2]), purity, joint_h, diag
+
+
+def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunReport:
+    """Execute a full ensemble run on the GPU(s) (ensemble.py:635-804)."""
+    import torch
+
+    if sinks is None:
+        sinks = MemorySinks()
+    profile = StageProfile()
+    io_seconds = 0.0
+    clock = time.perf_counter
+    wall_start = clock()
+
+    def emit(method, *args):
+        nonlocal io_seconds
+        t0 = clock()
+        method(*args)
+        io_seconds += clock() - t0
+
+    rank, world = sharding.world_info(group)
+    with profile.stage(STAGE_INITIALIZATION):
+        estimate = estimate_memory(config, world)
+        if estimate["total_bytes"] > config.memory_budget:
+            raise MemoryBudgetError(
+                f"estimated device working set {estimate['total_bytes']:,} bytes exceeds the budget "
+                f"of {config.memory_budget:,}; lower realizations, shrink the lattice, or raise memory_budget"
+            )
+        if config.stepper.backend == BACKEND_EIGEN:
+            raise ConfigurationError(
+                "the eigen backend (dense diagonalisation) is not on the B200 path; use 'taylor' or 'rk4'"
+            )
+        if not config.noise.is_static:
+            raise ConfigurationError(
+                "dynamic telegraph noise (rate > 0) is not on the B200 path yet; use rate = 0 (static disorder)"
+            )
+        if OBS_PURITY in config.observables:
+            work = float(config.realizations) ** 2 * config.space.dim
+            if work > PURITY_WORK_CAP:
+                raise CapacityError(
+                    f"purity needs R^2*D = {work:.3g} overlap multiply-adds per snapshot "
+                    f"(cap {PURITY_WORK_CAP:.3g}); drop it from observables"
+                )
+            if world > 1 and config.realizations * config.space.dim * 16 > PURITY_GATHER_CAP:
+                raise CapacityError("multi-GPU purity gathers all states; too large for this run")
+        build_topology(config.space)
+        device = config.device if config.device is not None else _default_device()
+        lo, hi = sharding.shard_bounds(config.realizations, world, rank)
+        with torch.cuda.device(device):
+            ens = EnsembleState(config, device, lo, hi)
+    if config.precision == PRECISION_SINGLE:
+        emit(sinks.message, "precision=single requested: the B200 path propagates in double")
+    emit(sinks.message,
+         f"run start: dim={config.space.dim} realizations={config.realizations} steps={config.steps} "
+         f"backend={config.stepper.backend} precision={config.precision} workers={world} "
+         f"snapshots={len(config.schedule)}")
+
+    snapshots = 0
+    max_deviation = 0.0
+    corrections = 0
+    event_total = 0
+    previous = 0
+    with torch.cuda.device(device):
+        for target in config.schedule:
+            span = target - previous
+            if span > 0:
+                t0 = clock()
+                ens.evolve(previous, span)
+                local = ens.stats()
+                merged = sharding.merge_segment_stats(sharding.gather_objects(local, group))
+                profile.add(STAGE_EVOLUTION, clock() - t0, calls=config.realizations * span)
+                # static noise: the Hamiltonian is generated on the fly, nothing to update
+                profile.add(STAGE_HAMILTONIAN, 0.0, calls=config.realizations * span)
+                if merged["failure"] is not None:
+                    dev, real, step = merged["failure"]
+                    emit(sinks.message,
+                         f"aborted: norm deviation {dev:.3e} at realization {real}, step {step}; "
+                         f"reduce the time step")
+                    raise NormFailureError(dev, realization=real, step=step)
+                corrections += merged["corrections"]
+                event_total += merged["event_count"]
+                max_deviation = max(max_deviation, merged["max_deviation"])
+                if merged["events"]:
+                    emit(sinks.norm_events,
+                         [NormEvent(deviation=d, corrected=c, realization=r, step=s)
+                          for d, c, r, s in merged["events"]])
+            previous = target
+            with profile.stage(STAGE_DENSITY):
+                pops, pr, purity, joint, diag = collect_observables(config, ens, group)
+                time_tag = target * config.stepper.dt
+                rows = _observable_rows(config, pops, pr, purity, joint)
+                rho = DiagonalDensity(diag=(diag / config.realizations).cpu().numpy(),
+                                      dim=config.space.dim, sample_count=config.realizations,
+                                      time_tag=float(time_tag), purity=purity, populations=pops,
+                                      participation_ratio=pr)
+            snapshots += 1
+            emit(sinks.observable_rows, rho.time_tag, rows)
+            emit(sinks.density_snapshot, rho, target)
+
+    report = RunReport(config=config, profile=profile, io_seconds=io_seconds,
+                       wall_seconds=clock() - wall_start, workers=world, snapshots=snapshots,
+                       max_norm_deviation=max_deviation, norm_corrections=corrections,
+                       norm_events=event_total, switch_count=0, memory_estimate=estimate)
+    emit(sinks.message,
+         f"run end: snapshots={snapshots} corrections={corrections} switches=0 "
+         f"max_norm_deviation={max_deviation:.3e}")
+    sinks.finish(report)
+    return report

@@ -1,0 +1,190 @@
+"""Hamiltonian model and the matrix-free apply (device).
+
+``CouplingModel`` keeps the reference's fields and validation
+(hamiltonian.py:30-72).  ``assemble_values`` returns a ``StencilValues``
+instead of the reference's ``(B, D, H+1)`` complex value table
+(hamiltonian.py:105-144): for the ring stencil that table is fully determined
+by the per-realization link couplings ``hop[x] = t + xi_link[x]`` and on-site
+noise ``xi_site[x]`` -- O(N) instead of O(N^m) per realization -- and the
+kernels regenerate every entry on the fly.  ``apply_values``
+(hamiltonian.py:195-223) runs ``ctqw_apply`` in the reference's accumulation
+order, bit-identical to it.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ConfigurationError
+
+_HANDLES: dict = {}
+
+
+@dataclass(frozen=True)
+class CouplingModel:
+    onsite_energy: float = 0.0
+    tunneling: float | tuple = 1.0
+    interaction: float = 0.0
+    hbar: float = 1.0
+
+    def __post_init__(self):
+        if isinstance(self.tunneling, (list, tuple, np.ndarray)):
+            object.__setattr__(self, "tunneling", tuple(float(v) for v in self.tunneling))
+            amps = self.tunneling
+        else:
+            object.__setattr__(self, "tunneling", float(self.tunneling))
+            amps = (self.tunneling,)
+        for name in ("onsite_energy", "interaction", "hbar"):
+            if not np.isfinite(getattr(self, name)):
+                raise ConfigurationError(f"{name} = {getattr(self, name)} must be finite")
+        if not all(np.isfinite(amps)):
+            raise ConfigurationError("tunneling amplitudes must be finite")
+        if self.hbar <= 0:
+            raise ConfigurationError(f"hbar = {self.hbar} must be > 0")
+
+    def tunneling_per_direction(self, q: int) -> np.ndarray:
+        if isinstance(self.tunneling, tuple):
+            if len(self.tunneling) != q:
+                raise ConfigurationError(f"{len(self.tunneling)} tunneling amplitudes for {q} directions")
+            return np.asarray(self.tunneling, dtype=np.float64)
+        return np.full(q, self.tunneling, dtype=np.float64)
+
+    def ring_tunneling(self) -> float:
+        return float(self.tunneling_per_direction(1)[0])
+
+
+def handle_for(m, n, onsite, tunneling, interaction, hbar, device=None):
+    """Cached ``native.Handle`` for a model on a device."""
+    import torch
+
+    from .native import Handle
+
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    key = (int(m), int(n), float(onsite), float(tunneling), float(interaction), float(hbar), int(device))
+    h = _HANDLES.get(key)
+    if h is None:
+        h = Handle(m, n, onsite, tunneling, interaction, hbar, device)
+        _HANDLES[key] = h
+    return h
+
+
+def model_handle(topology, model: CouplingModel, hbar=None, device=None):
+    return handle_for(topology.m, topology.n, model.onsite_energy, model.ring_tunneling(),
+                      model.interaction, model.hbar if hbar is None else hbar, device)
+
+
+@dataclass
+class StencilValues:
+    """Per-realization couplings of the ring operator (device tensors).
+
+    ``hop``: ``batch + (N,)`` float64, ``site``: same or None.  ``batch`` is
+    ``()`` for one Hamiltonian shared by every state, ``(B,)`` for a stack.
+    """
+
+    topology: object
+    model: CouplingModel
+    hop: object
+    site: object | None
+
+    @property
+    def batch(self) -> tuple:
+        return tuple(self.hop.shape[:-1])
+
+    @property
+    def dim(self) -> int:
+        return self.topology.dim
+
+
+def _device_array(x, device):
+    import torch
+
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.float64).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.float64)), device=device)
+
+
+def assemble_values(topology, model: CouplingModel, link_values=None, site_values=None,
+                    out=None, dtype=np.complex128) -> StencilValues:
+    """Stencil couplings from optional noise arrays (hamiltonian.py:105-144)."""
+    import torch
+
+    h = model_handle(topology, model)
+    dev = torch.device(f"cuda:{h.device}")
+    n = topology.n
+    has_link = link_values is not None and np.shape(link_values)[-1] != 0
+    has_site = site_values is not None and np.shape(site_values)[-1] != 0
+    batch = ()
+    if has_link:
+        batch = tuple(np.shape(link_values)[:-1])
+    if has_site:
+        batch = tuple(np.shape(site_values)[:-1])
+    count = int(np.prod(batch)) if batch else 1
+    noise_cols = []
+    if has_link:
+        if np.shape(link_values)[-1] != n:
+            raise ConfigurationError(f"link_values needs {n} entries per realization")
+        noise_cols.append(_device_array(link_values, dev).reshape(count, n))
+    if has_site:
+        if np.shape(site_values)[-1] != n:
+            raise ConfigurationError(f"site_values needs {n} entries per realization")
+        noise_cols.append(_device_array(site_values, dev).reshape(count, n))
+    hop = torch.empty((count, n), dtype=torch.float64, device=dev)
+    site = torch.empty((count, n), dtype=torch.float64, device=dev) if has_site else None
+    noise = torch.cat(noise_cols, dim=1).contiguous() if noise_cols else None
+    h.build_coefficients(noise, count, n if has_link else 0, n if has_site else 0, hop, site)
+    hop = hop.reshape(batch + (n,))
+    if site is not None:
+        site = site.reshape(batch + (n,))
+    return StencilValues(topology=topology, model=model, hop=hop, site=site)
+
+
+def as_state_stack(psi, device):
+    """(tensor (B, D) complex128 on device, restore-fn) for numpy or torch input."""
+    import torch
+
+    if isinstance(psi, torch.Tensor):
+        shape = tuple(psi.shape)
+        t = psi.to(device=device, dtype=torch.complex128).reshape(-1, shape[-1]).contiguous()
+        return t, (lambda out: out.reshape(shape)), shape
+    arr = np.asarray(psi)
+    shape = arr.shape
+    t = torch.as_tensor(np.ascontiguousarray(arr.reshape(-1, shape[-1]), dtype=np.complex128),
+                        device=device)
+    return t, (lambda out: out.reshape(shape).cpu().numpy()), shape
+
+
+def bind_values(h, values: StencilValues, count: int):
+    """Bind ``values`` for a batch of ``count`` states (broadcast or per row)."""
+    vb = values.batch
+    vcount = int(np.prod(vb)) if vb else 1
+    if vb == () or vcount == 1 and count == 1:
+        stride = 0
+    elif vcount == count:
+        stride = values.topology.n
+    else:
+        raise ConfigurationError(f"values batch {vb} does not match {count} states")
+    hop = values.hop.reshape(-1, values.topology.n)
+    site = values.site.reshape(-1, values.topology.n) if values.site is not None else None
+    h.bind(hop, site, vcount, stride)
+
+
+def apply_values(topology, values: StencilValues, psi, out=None, exact: bool = True):
+    """``H psi`` through the on-the-fly stencil (hamiltonian.py:195-223)."""
+    import torch
+
+    h = model_handle(topology, values.model)
+    dev = torch.device(f"cuda:{h.device}")
+    stack, restore, _ = as_state_stack(psi, dev)
+    if stack.shape[-1] != topology.dim:
+        raise ConfigurationError(f"state has {stack.shape[-1]} amplitudes, expected {topology.dim}")
+    result = torch.empty_like(stack)
+    bind_values(h, values, stack.shape[0])
+    h.apply(stack, result, stack.shape[0], exact)
+    res = restore(result)
+    if out is not None:
+        out[...] = res
+        return out
+    return res

@@ -1,0 +1,376 @@
+"""GPU parity: libctqw (through its C ABI) against the oracle and the golden fixtures.
+
+Tolerances: bit-exact for the noise draw (integer work) and, in ``exact``
+mode, for every propagation between renormalisation events; 1e-13 absolute
+on amplitudes once rescales happen (the squared norm is an einsum in the
+reference); 1e-10 relative on observable rows (the north-star bar); FMA mode
+within 1e-12.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import ctqw_oracle as orc
+from tests.conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without CUDA")
+    import paper_1612_00746_b200 as p
+    from paper_1612_00746_b200 import native
+
+    native.load_library()
+    return p
+
+
+def numpy_noise(seed, r0, count, levels, total):
+    return np.stack([np.random.default_rng((seed, r)).choice(np.asarray(levels, dtype=float), size=total)
+                     for r in range(r0, r0 + count)]) if total else np.zeros((count, 0))
+
+
+def make_handle(m, n, onsite=0.0, t=1.0, U=0.0, hbar=1.0):
+    from paper_1612_00746_b200.native import Handle
+
+    return Handle(m, n, onsite, t, U, hbar, 0)
+
+
+def device_case(m, n, B, target="both", seed=1234, onsite=0.2, t=1.0, U=0.7, hbar=1.0, levels=(-0.1, 0.1)):
+    """Handle + bound device coefficients + oracle stencil for the same noise."""
+    h = make_handle(m, n, onsite, t, U, hbar)
+    nl = n if target in ("tunneling", "both") else 0
+    ns = n if target in ("onsite", "both") else 0
+    noise = numpy_noise(seed, 0, B, levels, nl + ns)
+    dev = torch.device("cuda:0")
+    hop = torch.empty((B, n), dtype=torch.float64, device=dev)
+    site = torch.empty((B, n), dtype=torch.float64, device=dev) if ns else None
+    nz = torch.as_tensor(noise, device=dev).contiguous() if nl + ns else None
+    h.build_coefficients(nz, B, nl, ns, hop, site)
+    h.bind(hop, site, B, n)
+    st = orc.make_stencil(m, n, onsite, t, U, link=noise[:, :nl] if nl else None,
+                          site=noise[:, nl:] if ns else None, batch=B)
+    return h, st, (hop, site)
+
+
+def to_dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.complex128), device="cuda:0")
+
+
+def stepper(backend="taylor", order=4, dt=0.05, tol_norm=1e-6, tol_fail=1e-3, renormalize=True, exact=True):
+    from paper_1612_00746_b200.native import make_stepper
+
+    return make_stepper(backend, order, dt, tol_norm, tol_fail, renormalize, exact)
+
+
+def random_states(B, dim, seed=0):
+    rng = np.random.default_rng(seed)
+    psi = rng.normal(size=(B, dim)) + 1j * rng.normal(size=(B, dim))
+    return psi / np.linalg.norm(psi, axis=1, keepdims=True)
+
+
+# ---------------------------------------------------------------------------
+# noise draw (integer work: bit-exact)
+
+
+def test_noise_draw_matches_golden(pkg):
+    data, meta = load_golden("noise_draws.npz")
+    h = make_handle(1, 16)
+    for case in meta:
+        total = case["n_links"] + case["n_sites"]
+        out = torch.empty((1, total), dtype=torch.float64, device="cuda:0")
+        h.draw_noise(case["seed"], case["r"], 1, case["levels"], total, out)
+        np.testing.assert_array_equal(out.cpu().numpy()[0], data[case["key"]])
+
+
+def test_noise_draw_stack_matches_numpy(pkg):
+    h = make_handle(2, 64)
+    for levels in ((-0.1, 0.1), (-0.3, 0.0, 0.3), (1.0, 2.0, 3.0, 4.0, 5.0)):
+        out = torch.empty((300, 2048), dtype=torch.float64, device="cuda:0")
+        h.draw_noise(1234, 10, 300, levels, 2048, out)
+        ref = numpy_noise(1234, 10, 300, levels, 2048)
+        np.testing.assert_array_equal(out.cpu().numpy(), ref)
+
+
+# ---------------------------------------------------------------------------
+# single steps vs the reference's own outputs (golden)
+
+
+@pytest.mark.parametrize("idx", range(5))
+def test_apply_and_steps_bit_exact_vs_reference(pkg, idx):
+    data, meta = load_golden("stencil_steps.npz")
+    c = meta[idx]
+    h = make_handle(c["m"], c["n"], c["onsite"], c["tunneling"], c["interaction"], c["hbar"])
+    n, b = c["n"], c["b"]
+    dev = torch.device("cuda:0")
+    noise = torch.as_tensor(np.concatenate([data[f"link{idx}"], data[f"site{idx}"]], axis=1),
+                            device=dev).contiguous()
+    hop = torch.empty((b, n), dtype=torch.float64, device=dev)
+    site = torch.empty((b, n), dtype=torch.float64, device=dev)
+    h.build_coefficients(noise, b, n, n, hop, site)
+    h.bind(hop, site, b, n)
+    psi = to_dev(data[f"psi{idx}"])
+    out = torch.empty_like(psi)
+    h.apply(psi, out, b, exact=True)
+    np.testing.assert_array_equal(out.cpu().numpy(), data[f"apply{idx}"])
+    for key, st in ((f"taylor4_{idx}", stepper("taylor", 4, c["dt"])),
+                    (f"taylor7_{idx}", stepper("taylor", 7, c["dt"])),
+                    (f"rk4_{idx}", stepper("rk4", 4, c["dt"]))):
+        h.step(psi, out, b, st)
+        np.testing.assert_array_equal(out.cpu().numpy(), data[key], err_msg=key)
+    # tunnelling-only coefficients
+    hop_t = torch.empty((b, n), dtype=torch.float64, device=dev)
+    h.build_coefficients(torch.as_tensor(data[f"link{idx}"], device=dev).contiguous(), b, n, 0, hop_t, None)
+    h.bind(hop_t, None, b, n)
+    h.step(psi, out, b, stepper("taylor", 4, c["dt"]))
+    np.testing.assert_array_equal(out.cpu().numpy(), data[f"taylor4t_{idx}"])
+
+
+# ---------------------------------------------------------------------------
+# evolve: resident (N <= 64), streaming tile (N > 64), generic (m = 1, 3)
+
+
+def run_evolve(h, psi0, B, n_steps, st, first_step=0):
+    psi = to_dev(psi0)
+    work = torch.empty_like(psi)
+    swapped = h.evolve(psi, work, B, first_step, n_steps, st)
+    stats = h.segment_stats(0)
+    res = (work if swapped else psi).cpu().numpy()
+    return res, stats
+
+
+def assert_stats_match(stats, ostats):
+    assert stats.event_count == ostats.event_count
+    assert stats.corrections == ostats.corrections
+    assert stats.max_deviation == pytest.approx(ostats.max_deviation, rel=1e-9, abs=1e-15)
+    mine = [(int(e.realization), int(e.step), bool(e.corrected)) for e in stats.events[: stats.n_events]]
+    theirs = [(r, s, c) for _, c, r, s in ostats.events]
+    assert mine == theirs
+
+
+CASES = [
+    # (m, n, B, backend, order, dt, steps, target)
+    (2, 16, 5, "taylor", 4, 0.05, 60, "both"),      # resident, with rescales
+    (2, 64, 6, "taylor", 4, 0.02, 40, "tunneling"),  # resident, no rescale
+    (2, 64, 4, "rk4", 4, 0.05, 40, "both"),          # resident RK4
+    (2, 33, 3, "taylor", 6, 0.05, 30, "onsite"),     # resident, order 6
+    (2, 96, 3, "taylor", 4, 0.05, 30, "both"),       # tile, ragged last tile
+    (2, 128, 3, "taylor", 4, 0.02, 25, "tunneling"), # tile, exact fit
+    (2, 128, 2, "rk4", 4, 0.05, 25, "both"),         # tile RK4
+    (2, 80, 2, "taylor", 2, 0.03, 20, "both"),       # tile, order 2
+    (2, 72, 2, "taylor", 6, 0.03, 10, "both"),       # generic m=2 (order > 4)
+    (1, 40, 4, "taylor", 4, 0.1, 50, "both"),        # generic m=1
+    (3, 12, 3, "taylor", 4, 0.04, 30, "both"),       # generic m=3
+    (3, 10, 2, "rk4", 4, 0.04, 20, "tunneling"),     # generic m=3 RK4
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"m{c[0]}n{c[1]}{c[3]}{c[4]}" for c in CASES])
+def test_evolve_matches_oracle(pkg, case):
+    m, n, B, backend, order, dt, steps, target = case
+    h, st, _keep = device_case(m, n, B, target)
+    psi0 = np.tile(orc.product_state(m, n), (B, 1))
+    mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, order, dt))
+    ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, order)
+    assert not stats.failed
+    assert_stats_match(stats, ostats)
+    if ostats.event_count == 0:
+        np.testing.assert_array_equal(mine, ref)   # exact mode: reference bits
+    else:
+        assert np.abs(mine - ref).max() <= 1e-13
+
+
+@pytest.mark.parametrize("case", [CASES[1], CASES[5], CASES[10]], ids=["resident", "tile", "generic"])
+def test_fma_mode_close(pkg, case):
+    m, n, B, backend, order, dt, steps, target = case
+    h, st, _keep = device_case(m, n, B, target)
+    psi0 = np.tile(orc.product_state(m, n), (B, 1))
+    mine, _ = run_evolve(h, psi0, B, steps, stepper(backend, order, dt, exact=False))
+    ref, _ = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, order)
+    assert np.abs(mine - ref).max() <= 1e-12
+
+
+def test_segments_compose_and_repeat_bitwise(pkg):
+    """Two segments == one segment; a repeat run is bit-identical."""
+    for n in (48, 100):
+        h, st, _keep = device_case(2, n, 3, "both")
+        psi0 = np.tile(orc.product_state(2, n), (3, 1))
+        one, _ = run_evolve(h, psi0, 3, 30, stepper(dt=0.05))
+        a, _ = run_evolve(h, psi0, 3, 13, stepper(dt=0.05))
+        b, _ = run_evolve(h, a, 3, 17, stepper(dt=0.05), first_step=13)
+        np.testing.assert_array_equal(one, b)
+        again, _ = run_evolve(h, psi0, 3, 30, stepper(dt=0.05))
+        np.testing.assert_array_equal(one, again)
+
+
+def test_norm_failure_matches_reference(pkg):
+    data, _ = load_golden("segments.npz")
+    fail = json.loads(str(data["failure"]))
+    noise = numpy_noise(99, 0, 4, (-0.4, 0.4), 18)
+    h = make_handle(2, 9, 0.0, 1.0, 0.0, 1.0)
+    dev = torch.device("cuda:0")
+    hop = torch.empty((4, 9), dtype=torch.float64, device=dev)
+    site = torch.empty((4, 9), dtype=torch.float64, device=dev)
+    h.build_coefficients(torch.as_tensor(noise, device=dev).contiguous(), 4, 9, 9, hop, site)
+    h.bind(hop, site, 4, 9)
+    psi0 = np.zeros((4, 81), dtype=np.complex128)
+    psi0[:, 3 * 9 + 4] = 1.0
+    _, stats = run_evolve(h, psi0, 4, 50, stepper("taylor", 4, 0.6, renormalize=False))
+    assert stats.failed
+    assert stats.fail_realization == fail["realization"]
+    assert stats.fail_step == fail["step"]
+    assert stats.fail_deviation == pytest.approx(fail["deviation"], rel=1e-12)
+
+
+def test_tile_norm_failure(pkg):
+    """Streaming path reports the earliest failing step and the worst row."""
+    B, n = 3, 80
+    h, st, _keep = device_case(2, n, B, "both", levels=(-0.4, 0.4))
+    psi0 = np.tile(orc.product_state(2, n), (B, 1))
+    _, stats = run_evolve(h, psi0, B, 40, stepper(dt=0.6, renormalize=False))
+    with pytest.raises(orc.NormFailure) as info:
+        orc.evolve_segment(st, psi0.copy(), 0, 40, 0.6, renormalize=False)
+    assert stats.failed
+    assert stats.fail_step == info.value.step
+    assert stats.fail_realization == info.value.realization
+
+
+def test_check_norm_stack_semantics(pkg):
+    p = pkg
+    rng = np.random.default_rng(14)
+    stack = rng.normal(size=(6, 32)) + 1j * rng.normal(size=(6, 32))
+    stack /= np.linalg.norm(stack, axis=1, keepdims=True)
+    stack[1] *= 1.0 + 2e-4
+    stack[4] *= 1.0 - 3e-4
+    ref = stack.copy()
+    cfg = p.StepperConfig(tol_norm=1e-6, tol_fail=1e-1)
+    dev, corr = p.check_norm_stack(stack, cfg)
+    odev, ocorr = orc.check_norm_stack(ref, 1e-6, 1e-1)
+    assert corr.tolist() == ocorr.tolist() == [False, True, False, False, True, False]
+    np.testing.assert_allclose(dev, odev, rtol=1e-12, atol=1e-15)
+    assert np.abs(stack - ref).max() <= 1e-15
+    stack[2] *= 2.0
+    with pytest.raises(p.NormFailureError) as info:
+        p.check_norm_stack(stack, cfg)
+    assert info.value.realization == 2
+
+
+# ---------------------------------------------------------------------------
+# observables and run()
+
+
+def _initial(c):
+    if c["initial"] == "antisymmetrized_pair":
+        n = c["n"]
+        x = (n - 2) // 2
+        psi = np.zeros(n * n, dtype=np.complex128)
+        psi[x * n + x + 1] = 1 / np.sqrt(2.0)
+        psi[(x + 1) * n + x] = -1 / np.sqrt(2.0)
+        return psi
+    return orc.product_state(c["m"], c["n"])
+
+
+@pytest.mark.parametrize("idx", range(5))
+def test_run_rows_match_reference(pkg, idx):
+    p = pkg
+    data, meta = load_golden("run_rows.npz")
+    c = meta[idx]
+    cfg = p.RunConfig(
+        space=p.JointSpace(p.build_lattice([c["n"]]), c["m"]),
+        model=p.CouplingModel(onsite_energy=c["onsite"], tunneling=c["tunneling"], interaction=c["interaction"]),
+        noise=p.NoiseSpec(target=c["target"], levels=(-0.1, 0.1), rate=0.0),
+        stepper=p.StepperConfig(backend=c["backend"], dt=c["dt"]),
+        initial=p.InitialStateSpec(kind=c["initial"]),
+        realizations=c["R"], steps=c["steps"], post_rate=c["post_rate"], master_seed=1234,
+        precision="double", observables=c["observables"],
+    )
+    sinks = p.MemorySinks()
+    report = p.run(cfg, sinks)
+    assert [(t, n, i) for t, n, i, _ in sinks.rows] == [tuple(r) for r in c["rows"]]
+    mine = np.array([v for *_, v in sinks.rows])
+    np.testing.assert_allclose(mine, data[f"rows{idx}"], rtol=1e-10, atol=1e-13)
+    assert report.norm_corrections == c["corrections"]
+    assert report.norm_events == c["norm_events"]
+    assert report.snapshots == len(cfg.schedule)
+
+
+@pytest.mark.parametrize("n,R,backend", [(64, 20, "taylor"), (100, 6, "rk4"), (20, 5, "taylor")])
+def test_run_matches_oracle_rows(pkg, n, R, backend):
+    p = pkg
+    obs = ("populations", "position_mean_variance", "purity", "participation_ratio", "joint_distribution")
+    cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([n]), 2),
+                      model=p.CouplingModel(onsite_energy=0.1, interaction=0.3),
+                      noise=p.NoiseSpec(target="both", rate=0.0),
+                      stepper=p.StepperConfig(backend=backend, dt=0.04),
+                      realizations=R, steps=30, post_rate=10, precision="double", observables=obs)
+    sinks = p.MemorySinks()
+    p.run(cfg, sinks)
+    noise = numpy_noise(1234, 0, R, (-0.1, 0.1), 2 * n)
+    st = orc.make_stencil(2, n, 0.1, 1.0, 0.3, link=noise[:, :n], site=noise[:, n:], batch=R)
+    out, _, _ = orc.run_rows(st, orc.product_state(2, n), R, 30, 10, 0.04, backend=backend, observables=obs)
+    ref = [(t, name, i, v) for t, rr in out for name, i, v in rr]
+    assert [r[:3] for r in sinks.rows] == [r[:3] for r in ref]
+    np.testing.assert_allclose([r[3] for r in sinks.rows], [r[3] for r in ref], rtol=1e-10, atol=1e-14)
+
+
+def test_run_norm_failure_names_culprit(pkg):
+    p = pkg
+    cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([9]), 1), noise=p.NoiseSpec(levels=(0.0,), rate=0.0),
+                      stepper=p.StepperConfig(dt=2.5, renormalize=False), realizations=3, steps=10,
+                      post_rate=10, precision="double")
+    sinks = p.MemorySinks()
+    with pytest.raises(p.NormFailureError) as info:
+        p.run(cfg, sinks)
+    assert info.value.realization is not None and info.value.step is not None
+    assert "reduce the time step" in str(info.value)
+    assert any(m.startswith("aborted") for m in sinks.messages)
+
+
+# ---------------------------------------------------------------------------
+# size-independent properties at the BASELINE sizes
+
+
+def test_taylor_rk4_agree_at_n256(pkg):
+    B, n = 4, 256
+    h, _, _keep = device_case(2, n, B, "tunneling")
+    psi0 = np.tile(orc.product_state(2, n), (B, 1))
+    a, sa = run_evolve(h, psi0, B, 50, stepper("taylor", 4, 0.02))
+    b, sb = run_evolve(h, psi0, B, 50, stepper("rk4", 4, 0.02))
+    assert np.abs(a - b).max() <= 1e-13
+    norms = (np.abs(a) ** 2).sum(axis=1)
+    assert np.all(np.abs(norms - 1.0) < 1e-7)
+    assert sa.event_count == 0 and sb.event_count == 0
+
+
+def test_antisymmetric_exclusion_n512(pkg):
+    """Link noise is exchange symmetric: a fermionic pair never doubly occupies."""
+    B, n = 2, 512
+    h, _, _keep = device_case(2, n, B, "tunneling")
+    x = (n - 2) // 2
+    psi0 = np.zeros((B, n * n), dtype=np.complex128)
+    psi0[:, x * n + x + 1] = 1 / np.sqrt(2.0)
+    psi0[:, (x + 1) * n + x] = -1 / np.sqrt(2.0)
+    out, _ = run_evolve(h, psi0, B, 20, stepper(dt=0.02))
+    diag = out.reshape(B, n, n)[:, np.arange(n), np.arange(n)]
+    assert np.abs(diag).max() < 1e-12
+    # exchange antisymmetry holds realization by realization
+    grid = out.reshape(B, n, n)
+    assert np.abs(grid + grid.transpose(0, 2, 1)).max() < 1e-12
+
+
+def test_realization_independence_of_batching(pkg):
+    """A realization's result does not depend on which batch it ran in."""
+    B, n = 6, 128
+    h, _, _keep = device_case(2, n, B, "both")
+    psi0 = np.tile(orc.product_state(2, n), (B, 1))
+    full, _ = run_evolve(h, psi0, B, 12, stepper(dt=0.03))
+    hop, site = _keep
+    h.bind(hop[2:5], site[2:5], 3, n)
+    part, _ = run_evolve(h, psi0[2:5], 3, 12, stepper(dt=0.03))
+    np.testing.assert_array_equal(full[2:5], part)

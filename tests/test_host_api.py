@@ -1,0 +1,206 @@
+"""Host-side API (no GPU): configuration validation with the reference's error
+classes, schedules, initial states, memory estimate, and the C ABI library
+loading with every symbol ``include/ctqw.h`` declares."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1612_00746_b200 as p
+from paper_1612_00746_b200 import native, sharding
+from tests.conftest import ROOT
+
+
+def ring(n, m=1):
+    return p.JointSpace(lattice=p.build_lattice([n]), m=m)
+
+
+def cfg(**kw):
+    base = dict(space=ring(9), noise=p.NoiseSpec(levels=(0.0,), rate=0.0),
+                stepper=p.StepperConfig(dt=0.05), realizations=1, steps=20, post_rate=20,
+                precision="double")
+    base.update(kw)
+    return p.RunConfig(**base)
+
+
+def test_exit_codes_match_reference():
+    assert p.ConfigurationError.exit_code == 2
+    assert p.NumericError.exit_code == 3
+    assert p.NormFailureError.exit_code == 3
+    assert p.CapacityError.exit_code == 4
+    assert p.MemoryBudgetError.exit_code == 4
+    assert p.SnapshotFormatError.exit_code == 5
+    e = p.NormFailureError(2.5e-3, realization=7, step=12)
+    assert "realization 7, step 12" in str(e) and "reduce the time step" in str(e)
+    import pickle
+
+    e2 = pickle.loads(pickle.dumps(e))
+    assert (e2.deviation, e2.realization, e2.step) == (2.5e-3, 7, 12)
+
+
+def test_schedule_semantics():
+    assert cfg(steps=6, post_rate=2).schedule == (2, 4, 6)
+    assert cfg(steps=7, post_rate=3).schedule == (3, 6, 7)
+    assert cfg(steps=0, post_rate=10).schedule == (0,)
+    assert cfg(steps=1500, post_rate=1500).schedule == (1500,)
+
+
+@pytest.mark.parametrize("bad", [dict(post_rate=0), dict(steps=10, post_rate=11), dict(realizations=0),
+                                 dict(precision="half"), dict(observables=("entropy",)),
+                                 dict(observables=()), dict(memory_budget=0)])
+def test_run_config_validation(bad):
+    with pytest.raises(p.ConfigurationError):
+        cfg(**bad)
+
+
+def test_stepper_and_model_validation():
+    with pytest.raises(p.ConfigurationError):
+        p.StepperConfig(backend="verlet")
+    with pytest.raises(p.ConfigurationError):
+        p.StepperConfig(dt=0.0)
+    with pytest.raises(p.ConfigurationError):
+        p.StepperConfig(taylor_order=0)
+    with pytest.raises(p.ConfigurationError):
+        p.StepperConfig(tol_norm=1e-3, tol_fail=1e-6)
+    with pytest.raises(p.ConfigurationError):
+        p.CouplingModel(hbar=0.0)
+    with pytest.raises(p.ConfigurationError):
+        p.NoiseSpec(target="links")
+    with pytest.raises(p.ConfigurationError):
+        p.NoiseSpec(levels=())
+    with pytest.raises(p.ConfigurationError):
+        p.build_lattice([4], k_half=[2])
+    # the eigen backend validates but is rejected by the device path
+    with pytest.raises(p.ConfigurationError):
+        p.StepperConfig(backend="eigen").native()
+
+
+def test_default_observables_and_position_rule():
+    assert cfg().observables == ("populations", "position_mean_variance", "purity", "participation_ratio")
+    grid = p.JointSpace(p.build_lattice([3, 3]), 1)
+    assert "position_mean_variance" not in p.RunConfig(space=grid, steps=1, post_rate=1).observables
+    with pytest.raises(p.ConfigurationError):
+        p.RunConfig(space=grid, steps=1, post_rate=1, observables=("position_mean_variance",))
+
+
+def test_topology_scope():
+    assert p.build_topology(ring(7, 2)).dim == 49
+    with pytest.raises(p.ConfigurationError):
+        p.build_topology(p.JointSpace(p.build_lattice([3, 4]), 2))
+    with pytest.raises(p.ConfigurationError):
+        p.build_topology(p.JointSpace(p.build_lattice([8], boundary="open"), 1))
+    with pytest.raises(p.ConfigurationError):
+        p.build_topology(ring(5, 4))
+
+
+def test_initial_states():
+    space = ring(7, 2)
+    psi = p.build_initial_state(p.InitialStateSpec(), space)
+    assert psi[p.joint_index([2, 3], space)] == 1.0 and np.count_nonzero(psi) == 1
+    psi = p.build_initial_state(p.InitialStateSpec(kind="antisymmetrized_pair", positions=(1, 3)), ring(5, 2))
+    assert psi[p.joint_index([3, 1], ring(5, 2))] == pytest.approx(-1 / np.sqrt(2))
+    with pytest.raises(p.ConfigurationError):
+        p.build_initial_state(p.InitialStateSpec(kind="antisymmetrized_pair", positions=(2, 2)), ring(5, 2))
+    psi = p.build_initial_state(p.InitialStateSpec(kind="custom_vector", amplitudes=np.array([2, 0, 0, 2j])),
+                                ring(4))
+    assert np.linalg.norm(psi) == pytest.approx(1.0)
+    assert p.build_initial_state(p.InitialStateSpec(), ring(9))[4] == 1.0
+    space3 = ring(6, 3)
+    psi = p.build_initial_state(p.InitialStateSpec(kind="product", positions=(0, 0, 5)), space3)
+    assert psi[p.joint_index([0, 0, 5], space3)] == 1.0
+
+
+def test_joint_index_roundtrip():
+    space = ring(11, 3)
+    a = np.arange(space.dim)
+    np.testing.assert_array_equal(p.joint_index(p.joint_positions(a, space), space), a)
+
+
+def test_memory_estimate_and_budget():
+    est = p.estimate_memory(cfg(space=ring(256, 2), realizations=1000))
+    assert est["state_bytes"] == 2 * 1000 * 65536 * 16
+    assert est["topology_bytes"] == 0
+    assert p.estimate_memory(cfg(space=ring(256, 2), realizations=1000), world=8)["state_bytes"] == \
+        2 * 125 * 65536 * 16
+
+
+def test_run_rejects_out_of_scope_before_touching_device():
+    with pytest.raises(p.MemoryBudgetError):
+        p.run(cfg(memory_budget=16))
+    with pytest.raises(p.ConfigurationError):
+        p.run(cfg(stepper=p.StepperConfig(backend="eigen")))
+    with pytest.raises(p.ConfigurationError):
+        p.run(cfg(noise=p.NoiseSpec(rate=0.5)))
+    with pytest.raises(p.CapacityError):
+        p.run(cfg(space=ring(1024, 2), realizations=10000, memory_budget=2**50))
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(p.NativeError):
+        p.run(cfg())
+    with pytest.raises(p.NativeError):
+        native.Handle(2, 16, 0.0, 1.0, 0.0, 1.0)
+
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "ctqw.h")).read()
+    declared = set(re.findall(r"^\S.*?\b(ctqw_[a-z_0-9]+)\s*\(", header, flags=re.M))
+    assert declared == set(native.SIGNATURES), declared ^ set(native.SIGNATURES)
+    lib = native.load_library()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.ctqw_abi_version() == 1
+    assert native.exported_symbols() == list(native.SIGNATURES)
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", native.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_handle_create_errors_without_device():
+    """ctqw_create validates before touching CUDA."""
+    lib = native.load_library()
+    import ctypes
+
+    h = ctypes.c_void_p()
+    bad = native.Model(4, 16, 1, 1, 0.0, 1.0, 0.0, 1.0)
+    assert lib.ctqw_create(ctypes.byref(bad), 0, ctypes.byref(h)) == 2
+    bad = native.Model(2, 16, 2, 1, 0.0, 1.0, 0.0, 1.0)
+    assert lib.ctqw_create(ctypes.byref(bad), 0, ctypes.byref(h)) == 2
+    bad = native.Model(2, 16, 1, 1, 0.0, 1.0, 0.0, -1.0)
+    assert lib.ctqw_create(ctypes.byref(bad), 0, ctypes.byref(h)) == 2
+    assert b"hbar" in lib.ctqw_last_error(None)
+
+
+def test_shard_bounds_cover_realizations():
+    for R in (1, 7, 100, 1001):
+        for world in (1, 2, 3, 8):
+            shards = sharding.all_shards(R, world)
+            assert shards[0][0] == 0 and shards[-1][1] == R
+            assert all(a[1] == b[0] for a, b in zip(shards, shards[1:]))
+            sizes = [hi - lo for lo, hi in shards]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_merge_stats_first_failing_shard_wins():
+    a = {"event_count": 2, "corrections": 2, "max_deviation": 3e-6, "events": [(3e-6, True, 1, 5)],
+         "failure": None}
+    b = {"event_count": 1, "corrections": 1, "max_deviation": 2e-6, "events": [(2e-6, True, 9, 2)],
+         "failure": (5e-3, 9, 4)}
+    c = {"event_count": 0, "corrections": 0, "max_deviation": 0.0, "events": [], "failure": (9e-3, 12, 1)}
+    m = sharding.merge_segment_stats([a, b, c])
+    assert m["event_count"] == 3 and m["corrections"] == 3
+    assert m["max_deviation"] == 3e-6
+    assert m["events"] == [(3e-6, True, 1, 5), (2e-6, True, 9, 2)]
+    assert m["failure"] == (5e-3, 9, 4)
