@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -55,6 +56,7 @@ struct ctqw_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int64_t timed_launches = 0;
+  int stream_kind = 0;  // 0 band (default), 1 tile (CTQW_STREAM=tile)
   std::string err;
 };
 
@@ -302,6 +304,7 @@ int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
   }
   long long nf = kNoFail;
   cudaMemcpy(h->fail, &nf, sizeof(nf), cudaMemcpyHostToDevice);
+  if (const char* sk = std::getenv("CTQW_STREAM")) h->stream_kind = std::strcmp(sk, "tile") == 0 ? 1 : 0;
   *out = h;
   return CTQW_OK;
 }
@@ -509,8 +512,12 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
     return CTQW_OK;
   }
   if (!work) return fail_with(h, CTQW_ERR_CONFIG, "work buffer required");
-  if (tile_supported(h->m, h->n, sc)) {
-    const int nparts = tile_parts(h->n, sc);
+  // streaming m = 2 path: row-marching band kernel (default) or the v1 tile
+  // kernel (CTQW_STREAM=tile, kept for A/B measurements)
+  const bool use_band = band_supported(h->m, h->n, sc) && h->stream_kind != 1;
+  const bool use_tile = !use_band && tile_supported(h->m, h->n, sc);
+  if (use_band || use_tile) {
+    const int nparts = use_band ? band_parts(h->n, sc, coef.site != nullptr, count) : tile_parts(h->n, sc);
     rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
     if (rc) return rc;
     double2* bufs[2] = {psi, work};
@@ -518,8 +525,12 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       const double2* in = bufs[j & 1];
       double2* out = bufs[(j + 1) & 1];
       timing_event(h, s);
-      CUDA_TRY(h, launch_tile_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
-                                   h->fail, s));
+      if (use_band)
+        CUDA_TRY(h, launch_band_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
+                                     h->fail, s));
+      else
+        CUDA_TRY(h, launch_tile_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
+                                     h->fail, s));
       timing_event(h, s);
       h->timed_launches += h->timing ? 1 : 0;
       CUDA_TRY(h, launch_norm_decide(h->partial, nparts, count, (long long)(first_step + j + 1), pol,

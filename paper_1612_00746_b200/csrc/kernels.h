@@ -67,6 +67,13 @@ cudaError_t launch_tile_step(const double2* psi_in, double2* psi_out, int64_t co
                              const Coef& coef, const StencilConst& k, const StepScalars& sc,
                              bool exact, const double* scl, double* partial,
                              const long long* fail, cudaStream_t s);
+// step_band.cu (m = 2 row-marching streaming kernel)
+bool band_supported(int m, int n, const StepScalars& sc);
+int band_parts(int n, const StepScalars& sc, bool site, int64_t count);
+cudaError_t launch_band_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
+                             const Coef& coef, const StencilConst& k, const StepScalars& sc,
+                             bool exact, const double* scl, double* partial,
+                             const long long* fail, cudaStream_t s);
 cudaError_t launch_resident(double2* psi, int64_t count, int n, const Coef& coef,
                             const StencilConst& k, const StepScalars& sc, bool exact,
                             const NormPolicy& pol, long long first_step, long long n_steps,

@@ -165,6 +165,11 @@ CASES = [
     (2, 128, 3, "taylor", 4, 0.02, 25, "tunneling"), # tile, exact fit
     (2, 128, 2, "rk4", 4, 0.05, 25, "both"),         # tile RK4
     (2, 80, 2, "taylor", 2, 0.03, 20, "both"),       # tile, order 2
+    (2, 600, 1, "taylor", 4, 0.02, 6, "both"),       # band, 2 haloed x-bands
+    (2, 100, 3, "rk4", 4, 0.05, 12, "both"),         # band, haloed single band, RK4
+    (2, 160, 2, "taylor", 3, 0.04, 15, "onsite"),    # band full row, order 3
+    (2, 256, 2, "taylor", 1, 0.005, 15, "both"),     # band full row, order 1
+    (2, 512, 1, "rk4", 4, 0.03, 4, "tunneling"),     # band full row, 512 threads
     (2, 72, 2, "taylor", 6, 0.03, 10, "both"),       # generic m=2 (order > 4)
     (1, 40, 4, "taylor", 4, 0.1, 50, "both"),        # generic m=1
     (3, 12, 3, "taylor", 4, 0.04, 30, "both"),       # generic m=3
