@@ -65,35 +65,65 @@ def parse():
 # CPU side (oracle port = the reference's algorithm, NumPy)
 
 
+_WORKER_STATE = {}
+
+
 def _cpu_worker(args):
+    """One task = ``count`` realizations advanced ``steps`` steps by the oracle.
+
+    The realization stack persists in the worker process between tasks (like
+    the reference's per-worker chunks), so only stepping is timed.
+    """
     n, m, count, r0, steps, dt, backend, order = args
     import numpy as np
 
     from oracle import ctqw_oracle as orc
 
-    noise = np.stack([np.random.default_rng((1234, r)).choice(np.array([-0.1, 0.1]), n)
-                      for r in range(r0, r0 + count)])
-    st = orc.make_stencil(m, n, 0.0, 1.0, 0.0, link=noise, batch=count)
-    psi = np.tile(orc.product_state(m, n), (count, 1))
+    key = (n, m, count, backend, order, dt)
+    st_psi = _WORKER_STATE.get(key)
+    if st_psi is None:
+        noise = np.stack([np.random.default_rng((1234, r)).choice(np.array([-0.1, 0.1]), n)
+                          for r in range(r0, r0 + count)])
+        st = orc.make_stencil(m, n, 0.0, 1.0, 0.0, link=noise, batch=count)
+        st_psi = (st, np.tile(orc.product_state(m, n), (count, 1)), 0)
+    st, psi, done = st_psi
     t0 = time.perf_counter()
-    orc.evolve_segment(st, psi, 0, steps, dt, 1.0, backend, order)
+    psi, _ = orc.evolve_segment(st, psi, done, steps, dt, 1.0, backend, order)
+    _WORKER_STATE[key] = (st, psi, done + steps)
     return time.perf_counter() - t0
 
 
-def cpu_rate(n, m, backend, order, dt, per_core, steps, cores=None):
-    """Wall rate of the oracle on ``cores`` processes (OPENBLAS 1 thread each)."""
-    from concurrent.futures import ProcessPoolExecutor
-    import multiprocessing as mp
+class CpuPool:
+    """Persistent spawn pool of ``cores`` processes (1 BLAS thread each)."""
 
-    cores = cores or host_cores()
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    jobs = [(n, m, per_core, 100000 + i * per_core, steps, dt, backend, order) for i in range(cores)]
-    with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as pool:
-        list(pool.map(_cpu_worker, [(n, m, 1, 0, 1, dt, backend, order)] * cores))  # warm imports
+    def __init__(self, cores):
+        from concurrent.futures import ProcessPoolExecutor
+        import multiprocessing as mp
+
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        self.cores = cores
+        self.pool = ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn"))
+
+    def step(self, n, m, backend, order, dt, per_core, steps):
+        jobs = [(n, m, per_core, 100000 + i * per_core, steps, dt, backend, order) for i in range(self.cores)]
         t0 = time.perf_counter()
-        list(pool.map(_cpu_worker, jobs))
-        wall = time.perf_counter() - t0
+        list(self.pool.map(_cpu_worker, jobs))
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.shutdown(wait=True)
+
+
+def cpu_rate(n, m, backend, order, dt, per_core, steps, cores=None):
+    """Wall rate of the oracle on ``cores`` processes over one timed task round."""
+    cores = cores or host_cores()
+    pool = CpuPool(cores)
+    try:
+        pool.step(n, m, backend, order, dt, per_core, 1)  # imports + state set-up
+        wall = pool.step(n, m, backend, order, dt, per_core, steps)
+    finally:
+        pool.close()
     return cores * per_core * steps / wall, cores, wall
 
 
@@ -118,18 +148,19 @@ def reference_arm(a):
     if rank != 0:
         return
     cores = host_cores()
-    per_core, _ = cpu_sample_size(a.n, a.m, 2.0, cores)
-    per_core = max(1, min(per_core, 4))
-    rates = []
-    for _ in range(a.warmup):
-        cpu_rate(a.n, a.m, a.backend, a.order, a.dt, per_core, 1, cores)
-    t_all = 0.0
-    for _ in range(a.steps):
-        r, _, wall = cpu_rate(a.n, a.m, a.backend, a.order, a.dt, per_core, 1, cores)
-        rates.append(r)
-        t_all += wall
+    per_core = 2 if a.n ** a.m >= 65536 else 8
+    pool = CpuPool(cores)
+    try:
+        for _ in range(max(a.warmup, 1)):
+            pool.step(a.n, a.m, a.backend, a.order, a.dt, per_core, 1)
+        t_all = 0.0
+        for _ in range(a.steps):
+            t_all += pool.step(a.n, a.m, a.backend, a.order, a.dt, per_core, 1)
+    finally:
+        pool.close()
     value = a.steps * cores * per_core / t_all
-    sample = f"{cores} processes x {per_core} realizations x 1 step per timed step (N={a.n}, m={a.m})"
+    sample = (f"{cores} processes x {per_core} realizations advanced 1 step per timed step "
+              f"(N={a.n}, m={a.m}; oracle port of ctqw._evolve_segment)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * t_all / a.steps,
@@ -160,27 +191,55 @@ def workload_config(a):
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled through NVML every ~10 ms while
+    the timed region runs (falls back to nvidia-smi if NVML is missing)."""
+
+    REASONS = {  # nvmlClocksEventReason* bit -> name used in the JSON line
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reason_bits)
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._loop, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            try:
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            return float(sm), float(mx), int(bits)
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        return float(out[0]), float(out[1]), int(out[2].strip(), 16)
 
     def _loop(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -192,15 +251,15 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        bits = 0
+        for _, _, b in self.samples:
+            bits |= b
+        reasons = sorted(name for bit, name in self.REASONS.items() if bits & bit)
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def measured_peak_hbm():
@@ -295,9 +354,17 @@ def ours(a):
     achieved = bytes_per_launch / (avg_launch_ms / 1000.0) / 1e9
     peak, peak_src = measured_peak_hbm()
     traffic = ncu_traffic()
+    kernel = "band_ws_kernel" if a.n > 64 else "resident_kernel"
+    if os.environ.get("CTQW_STREAM") == "tile" and a.n > 64:
+        kernel = "tile_step_kernel"
+    traffic_bytes = None
+    if traffic and traffic.get("kernel") == kernel and a.n == 256 and a.m == 2:
+        # ncu --set full capture (profiles/), per realization-step, scaled to this launch
+        traffic_bytes = traffic["dram_bytes_per_realization_step"] * (hi - lo)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic.get("bytes_per_launch") if traffic else None,
-                "kernel": "tile_step_kernel" if a.n > 64 else "resident_kernel",
+                "frac": achieved / peak, "traffic": traffic_bytes,
+                "traffic_source": traffic.get("source") if traffic_bytes else None,
+                "kernel": kernel,
                 "kernel_ms_avg": avg_launch_ms, "kernel_launches": kernel_launches,
                 "kernel_share_of_step": kernel_ms / ms if ms > 0 else None,
                 "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
