@@ -514,10 +514,13 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   if (!work) return fail_with(h, CTQW_ERR_CONFIG, "work buffer required");
   // streaming m = 2 path: row-marching band kernel (default) or the v1 tile
   // kernel (CTQW_STREAM=tile, kept for A/B measurements)
-  const bool use_band = band_supported(h->m, h->n, sc) && h->stream_kind != 1;
-  const bool use_tile = !use_band && tile_supported(h->m, h->n, sc);
-  if (use_band || use_tile) {
-    const int nparts = use_band ? band_parts(h->n, sc, coef.site != nullptr, count) : tile_parts(h->n, sc);
+  const bool use_band2 = band2_supported(h->m, h->n, sc, exact) && h->stream_kind != 1;
+  const bool use_band = !use_band2 && band_supported(h->m, h->n, sc) && h->stream_kind != 1;
+  const bool use_tile = !use_band2 && !use_band && tile_supported(h->m, h->n, sc);
+  if (use_band2 || use_band || use_tile) {
+    const int nparts = use_band2 ? band2_parts(h->n, sc, coef.site != nullptr, count)
+                       : use_band ? band_parts(h->n, sc, coef.site != nullptr, count)
+                                  : tile_parts(h->n, sc);
     rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
     if (rc) return rc;
     double2* bufs[2] = {psi, work};
@@ -525,7 +528,10 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       const double2* in = bufs[j & 1];
       double2* out = bufs[(j + 1) & 1];
       timing_event(h, s);
-      if (use_band)
+      if (use_band2)
+        CUDA_TRY(h, launch_band2_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
+                                      h->fail, s));
+      else if (use_band)
         CUDA_TRY(h, launch_band_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
                                      h->fail, s));
       else
@@ -660,13 +666,13 @@ int ctqw_overlap_sumsq(ctqw_handle_t h, const double* a_dev, int64_t count_a, co
   if (count_a <= 0 || count_b <= 0) return fail_with(h, CTQW_ERR_CONFIG, "empty state stack");
   DeviceGuard g(h->device);
   const bool same = a_dev == b_dev && count_a == count_b;
-  const int64_t parts = overlap_parts(count_a, count_b, same);
-  int rc = ensure(h, &h->overlap_partial, &h->overlap_cap, parts, "overlap partials");
+  const int64_t need = overlap_scratch_doubles(count_a, count_b, same, h->dim) + 2;
+  int rc = ensure(h, &h->overlap_partial, &h->overlap_cap, need, "overlap partials");
   if (rc) return rc;
   CUDA_TRY(h, launch_overlap_sumsq((const double2*)a_dev, count_a, (const double2*)b_dev, count_b,
                                    h->dim, h->overlap_partial, h->overlap_cap, sumsq_dev,
                                    (cudaStream_t)stream));
-  h->launches += 2;
+  h->launches += 3;
   return CTQW_OK;
 }
 

@@ -67,6 +67,13 @@ cudaError_t launch_tile_step(const double2* psi_in, double2* psi_out, int64_t co
                              const Coef& coef, const StencilConst& k, const StepScalars& sc,
                              bool exact, const double* scl, double* partial,
                              const long long* fail, cudaStream_t s);
+// step_band2.cu (m = 2 row-marching kernel, two columns per thread)
+bool band2_supported(int m, int n, const StepScalars& sc, bool exact);
+int band2_parts(int n, const StepScalars& sc, bool site, int64_t count);
+cudaError_t launch_band2_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
+                              const Coef& coef, const StencilConst& k, const StepScalars& sc,
+                              bool exact, const double* scl, double* partial,
+                              const long long* fail, cudaStream_t s);
 // step_band.cu (m = 2 row-marching streaming kernel)
 bool band_supported(int m, int n, const StepScalars& sc);
 int band_parts(int n, const StepScalars& sc, bool site, int64_t count);
@@ -109,8 +116,9 @@ cudaError_t launch_observe_reduce(int m, int n, int64_t dim, const double* diag_
                                   double total, double* pops, double* scalars, double* joint,
                                   double* scratch, cudaStream_t s);
 cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b, int64_t rb,
-                                 int64_t dim, double* partial, int64_t nparts_cap,
+                                 int64_t dim, double* scratch, int64_t scratch_cap,
                                  double* out, cudaStream_t s);
 int64_t overlap_parts(int64_t ra, int64_t rb, bool same);
+int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim);
 
 }  // namespace ctqw

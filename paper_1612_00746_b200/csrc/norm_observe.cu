@@ -207,34 +207,35 @@ __global__ void joint_final_kernel(const double* __restrict__ partial, int npart
   scalars[2] = s2 > 0.0 ? (s1 * s1) / s2 : 0.0;
 }
 
-// sum_{i,j} |<a_i|b_j>|^2 : 32 x 32 blocks of the overlap matrix, each
-// thread a 2 x 2 sub-block, D swept in chunks staged through shared memory.
+// sum_{i,j} |<a_i|b_j>|^2 : 32 x 32 tiles of the overlap matrix G = A^H B,
+// each thread a 2 x 2 sub-block, D split over `ksplit` blocks per tile
+// (partial G tiles summed in a fixed order afterwards -> deterministic).
 constexpr int kOT = 32;   // overlap tile
-constexpr int kOK = 16;   // D chunk
+constexpr int kOK = 16;   // D chunk staged through shared memory
 
-__global__ void __launch_bounds__(256) overlap_kernel(const double2* __restrict__ a, int64_t ra,
-                                                      const double2* __restrict__ b, int64_t rb,
-                                                      int64_t dim, int same, int64_t ntj,
-                                                      double* partial) {
+__global__ void __launch_bounds__(256) overlap_partial_kernel(const double2* __restrict__ a, int64_t ra,
+                                                              const double2* __restrict__ b, int64_t rb,
+                                                              int64_t dim, int same, int64_t ntj,
+                                                              int64_t kspan, double2* __restrict__ gpart) {
   __shared__ double2 sa[kOK][kOT + 1];
   __shared__ double2 sb[kOK][kOT + 1];
-  __shared__ double red[32];
-  const int64_t ti = blockIdx.x / ntj, tj = blockIdx.x % ntj;
+  const int64_t tile = blockIdx.x;
+  const int64_t ti = tile / ntj, tj = tile % ntj;
+  const int ks = blockIdx.y;
   const int tid = threadIdx.x;
-  if (same && tj < ti) {
-    if (tid == 0) partial[blockIdx.x] = 0.0;
-    return;
-  }
+  if (same && tj < ti) return;
   const int li = (tid / 16) * 2, lj = (tid % 16) * 2;
   double2 g[2][2];
   for (int u = 0; u < 2; ++u)
     for (int v = 0; v < 2; ++v) g[u][v] = make_double2(0.0, 0.0);
-  for (int64_t k0 = 0; k0 < dim; k0 += kOK) {
+  const int64_t klo = ks * kspan;
+  const int64_t khi = klo + kspan < dim ? klo + kspan : dim;
+  for (int64_t k0 = klo; k0 < khi; k0 += kOK) {
     for (int e = tid; e < kOK * kOT; e += 256) {
       const int kk = e % kOK, rr = e / kOK;
       const int64_t gi = ti * kOT + rr, gj = tj * kOT + rr, gk = k0 + kk;
-      sa[kk][rr] = (gi < ra && gk < dim) ? a[gi * dim + gk] : make_double2(0.0, 0.0);
-      sb[kk][rr] = (gj < rb && gk < dim) ? b[gj * dim + gk] : make_double2(0.0, 0.0);
+      sa[kk][rr] = (gi < ra && gk < khi) ? a[gi * dim + gk] : make_double2(0.0, 0.0);
+      sb[kk][rr] = (gj < rb && gk < khi) ? b[gj * dim + gk] : make_double2(0.0, 0.0);
     }
     __syncthreads();
 #pragma unroll
@@ -251,11 +252,29 @@ __global__ void __launch_bounds__(256) overlap_kernel(const double2* __restrict_
     }
     __syncthreads();
   }
-  double s = 0.0;
+  double2* out = gpart + ((tile * gridDim.y + ks) * 256 + tid) * 4;
   for (int u = 0; u < 2; ++u)
-    for (int v = 0; v < 2; ++v) s += norm2(g[u][v]);
-  const double tot = block_sum(s, red);
-  if (tid == 0) partial[blockIdx.x] = (same && tj > ti) ? 2.0 * tot : tot;
+    for (int v = 0; v < 2; ++v) out[u * 2 + v] = g[u][v];
+}
+
+__global__ void __launch_bounds__(256) overlap_finish_kernel(const double2* __restrict__ gpart, int ksplit,
+                                                             int same, int64_t ntj, double* partial) {
+  __shared__ double red[32];
+  const int64_t tile = blockIdx.x;
+  const int64_t ti = tile / ntj, tj = tile % ntj;
+  const int tid = threadIdx.x;
+  if (same && tj < ti) {
+    if (tid == 0) partial[tile] = 0.0;
+    return;
+  }
+  double sq = 0.0;
+  for (int q = 0; q < 4; ++q) {
+    double2 g = make_double2(0.0, 0.0);
+    for (int ks = 0; ks < ksplit; ++ks) g = cadd(g, gpart[((tile * ksplit + ks) * 256 + tid) * 4 + q]);
+    sq += norm2(g);
+  }
+  const double tot = block_sum(sq, red);
+  if (tid == 0) partial[tile] = (same && tj > ti) ? 2.0 * tot : tot;
 }
 
 __global__ void sum_kernel(const double* __restrict__ partial, int64_t nparts, double* out) {
@@ -338,21 +357,43 @@ cudaError_t launch_observe_reduce(int m, int n, int64_t dim, const double* diag_
   return cudaGetLastError();
 }
 
+static int overlap_ksplit(int64_t ra, int64_t rb, bool same, int64_t dim) {
+  const int64_t ti = (ra + kOT - 1) / kOT, tj = (rb + kOT - 1) / kOT;
+  const int64_t active = same ? ti * (ti + 1) / 2 : ti * tj;
+  int64_t ks = (296 + active - 1) / active;
+  const int64_t kmax = dim / 256 > 0 ? dim / 256 : 1;
+  if (ks > kmax) ks = kmax;
+  if (ks > 64) ks = 64;
+  return (int)(ks < 1 ? 1 : ks);
+}
+
 int64_t overlap_parts(int64_t ra, int64_t rb, bool same) {
   (void)same;
   const int64_t ti = (ra + kOT - 1) / kOT, tj = (rb + kOT - 1) / kOT;
   return ti * tj;
 }
 
+int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim) {
+  const int64_t tiles = overlap_parts(ra, rb, same);
+  return tiles + tiles * overlap_ksplit(ra, rb, same, dim) * 256 * 4 * 2;
+}
+
 cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b, int64_t rb,
-                                 int64_t dim, double* partial, int64_t nparts_cap, double* out,
+                                 int64_t dim, double* scratch, int64_t scratch_cap, double* out,
                                  cudaStream_t s) {
   const bool same = (a == b) && (ra == rb);
   const int64_t ntj = (rb + kOT - 1) / kOT;
-  const int64_t nparts = overlap_parts(ra, rb, same);
-  if (nparts > nparts_cap) return cudaErrorInvalidValue;
-  overlap_kernel<<<(unsigned)nparts, 256, 0, s>>>(a, ra, b, rb, dim, same ? 1 : 0, ntj, partial);
-  sum_kernel<<<1, 1024, 0, s>>>(partial, nparts, out);
+  const int64_t tiles = overlap_parts(ra, rb, same);
+  const int ks = overlap_ksplit(ra, rb, same, dim);
+  if (overlap_scratch_doubles(ra, rb, same, dim) > scratch_cap) return cudaErrorInvalidValue;
+  double* partial = scratch;
+  double2* gpart = reinterpret_cast<double2*>(scratch + ((tiles + 1) & ~int64_t(1)));
+  int64_t kspan = (dim + ks - 1) / ks;
+  kspan = ((kspan + kOK - 1) / kOK) * kOK;
+  overlap_partial_kernel<<<dim3((unsigned)tiles, (unsigned)ks), 256, 0, s>>>(a, ra, b, rb, dim, same ? 1 : 0, ntj,
+                                                                             kspan, gpart);
+  overlap_finish_kernel<<<(unsigned)tiles, 256, 0, s>>>(gpart, ks, same ? 1 : 0, ntj, partial);
+  sum_kernel<<<1, 1024, 0, s>>>(partial, tiles, out);
   return cudaGetLastError();
 }
 

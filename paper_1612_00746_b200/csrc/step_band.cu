@@ -395,7 +395,7 @@ __device__ __forceinline__ void ws_iter_a(const BandArgs& a, const BandThread& T
   constexpr int P0 = PH % 3, P1 = (PH + 1) % 3, P2 = (PH + 2) % 3;
   const double c13 = 1.0 / 3.0, c16 = 1.0 / 6.0;
   const int n = a.n, NT = T.NT;
-  const double* hj = T.hopx + j;
+  const double2* hj = T.hop2 + j;
   const double* sj = T.sitex + j;
 #pragma unroll
   for (int k = KA; k >= 2; --k) {
@@ -406,7 +406,7 @@ __device__ __forceinline__ void ws_iter_a(const BandArgs& a, const BandThread& T
     const int gy = wrap_row(rr, n);
     double v0 = gy == T.gx ? a.k.base[1] : a.k.base[0];
     if (SITE) v0 = __dadd_rn(v0, __dadd_rn(sj[1 - 2 * k], T.sx));
-    const double2 h = stencil5<EXACT>(v0, up, mid, dn, lf, rt, hj[1 - 2 * k], hj[-2 * k], T.hx, T.hxm);
+    const double2 h = stencil5<EXACT>(v0, up, mid, dn, lf, rt, hj[1 - 2 * k].y, hj[1 - 2 * k].x, T.hx, T.hxm);
     const double2 st = times_i(RK4 ? a.ci[0] : a.ci[k - 1], h);
     const int AS = ((PH - 2 * k + 2) % NA + NA) % NA;
     double2 newt;
@@ -432,7 +432,7 @@ __device__ __forceinline__ void ws_iter_a(const BandArgs& a, const BandThread& T
   double v0 = gy == T.gx ? a.k.base[1] : a.k.base[0];
   if (SITE) v0 = __dadd_rn(v0, __dadd_rn(sj[-1], T.sx));
   const double2 mid = win[0][P2];
-  const double2 h = stencil5<EXACT>(v0, win[0][P1], mid, pj, lf, rt, hj[-1], hj[-2], T.hx, T.hxm);
+  const double2 h = stencil5<EXACT>(v0, win[0][P1], mid, pj, lf, rt, hj[-1].y, hj[-1].x, T.hx, T.hxm);
   const double2 st = times_i(a.ci[0], h);
   double2 newt, newacc;
   if (!RK4) {
@@ -460,7 +460,7 @@ __device__ __forceinline__ void ws_iter_b(const BandArgs& a, const BandThread& T
   constexpr int P0 = PH % 3, P1 = (PH + 1) % 3, P2 = (PH + 2) % 3;
   const double c13 = 1.0 / 3.0, c16 = 1.0 / 6.0;
   const int n = a.n, NT = T.NT;
-  const double* hj = T.hopx + j;
+  const double2* hj = T.hop2 + j;
   const double* sj = T.sitex + j;
   // newest t_KA row (produced by A last iteration)
   win[0][P2] = T.rowc[((KA - 1) * 3 + P2) * NT];
@@ -477,7 +477,7 @@ __device__ __forceinline__ void ws_iter_b(const BandArgs& a, const BandThread& T
     const int gy = wrap_row(rr, n);
     double v0 = gy == T.gx ? a.k.base[1] : a.k.base[0];
     if (SITE) v0 = __dadd_rn(v0, __dadd_rn(sj[1 - 2 * k], T.sx));
-    const double2 h = stencil5<EXACT>(v0, up, mid, dn, lf, rt, hj[1 - 2 * k], hj[-2 * k], T.hx, T.hxm);
+    const double2 h = stencil5<EXACT>(v0, up, mid, dn, lf, rt, hj[1 - 2 * k].y, hj[1 - 2 * k].x, T.hx, T.hxm);
     const double2 st = times_i(RK4 ? a.ci[0] : a.ci[k - 1], h);
     const int AS = ((PH - 2 * (k - KA - 1)) % NB + NB) % NB;
     if (k == NAPP) {
@@ -553,7 +553,8 @@ __global__ void __launch_bounds__(512, 1) band_ws_kernel(const __grid_constant__
   double2* ring = reinterpret_cast<double2*>(smem_raw);   // [RING][NT]
   double2* rows = ring + RING * NT;                      // [NAPP-1][3][NT]
   double2* acch = rows + NROWBUF * NT;                   // [3][NT]
-  double* hopx = reinterpret_cast<double*>(acch + 3 * NT);
+  double2* hop2 = acch + 3 * NT;                         // (hop[r-1], hop[r])
+  double* hopx = reinterpret_cast<double*>(hop2 + n + 2 * X);
   double* sitex = hopx + n + 2 * X;
   double* red = sitex + (SITE ? n + 2 * X : 0);
 
@@ -572,6 +573,7 @@ __global__ void __launch_bounds__(512, 1) band_ws_kernel(const __grid_constant__
   for (int i = tid; i < n + 2 * X; i += blockDim.x) {
     const int g = wrap(i - X, n);
     hopx[i] = hop[g];
+    hop2[i] = make_double2(hop[g == 0 ? n - 1 : g - 1], hop[g]);
     if (SITE) sitex[i] = site[g];
   }
   BandThread T;
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(512, 1) band_ws_kernel(const __grid_constant__
   T.dl = cl - c;
   T.dr = cr - c;
   T.hopx = hopx + X;
-  T.hop2 = nullptr;
+  T.hop2 = hop2 + X;
   T.sitex = sitex + X;
   T.edl = T.edr = nullptr;
   T.edw = nullptr;
@@ -711,6 +713,7 @@ BandPlan plan_band(int n, int napp, bool site, int64_t count, int num_sms) {
   if (p.ws) {
     // two thread groups of `threads` columns each; 32-row ring
     p.smem = (size_t)32 * p.threads * sizeof(double2) + (size_t)(rows * 3 + 3) * p.threads * sizeof(double2) +
+             (size_t)(n + 2 * kCoefPad) * sizeof(double2) +
              (size_t)((n + 2 * kCoefPad) * (site ? 2 : 1) + 32) * sizeof(double);
   } else {
     const int ES = napp > 1 ? (napp - 1) * 3 : 1;

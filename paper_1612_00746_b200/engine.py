@@ -393,8 +393,48 @@ def _observable_rows(config, pops, pr, purity, joint):
     return rows
 
 
-def collect_observables(config, ens: EnsembleState, group=None, want_joint=None):
-    """Device reduction of one collection point -> (pops, pr, purity, joint, diag)."""
+class PendingObservables:
+    """Observables of one collection point, enqueued on the device.
+
+    Everything the rows need is packed into one small device buffer
+    ``[populations (N) | sum p, sum p^2, PR | sum |<r|s>|^2]`` so reading the
+    rows costs one device-to-host copy; the diagonal and the joint
+    distribution stay on the device until asked for.
+    """
+
+    def __init__(self, config, packed, diag, joint, n):
+        self.config = config
+        self.packed = packed
+        self.diag_dev = diag
+        self.joint_dev = joint
+        self.n = n
+        self._host = None
+
+    def host(self):
+        if self._host is None:
+            self._host = self.packed.cpu().numpy()
+        return self._host
+
+    @property
+    def populations(self):
+        return self.host()[: self.n].copy()
+
+    @property
+    def participation_ratio(self):
+        return float(self.host()[self.n + 2])
+
+    @property
+    def purity(self):
+        if OBS_PURITY not in self.config.observables:
+            return None
+        return float(self.host()[self.n + 3]) / float(self.config.realizations) ** 2
+
+    def joint(self):
+        return self.joint_dev.cpu().numpy() if self.joint_dev is not None else None
+
+
+def collect_observables_async(config, ens: EnsembleState, group=None, want_joint=None):
+    """Enqueue one collection point (diagonal sum, all-reduce, reductions, purity)."""
     import torch
 
     space = config.space
@@ -406,21 +446,20 @@ def collect_observables(config, ens: EnsembleState, group=None, want_joint=None)
     else:
         diag.zero_()
     sharding.allreduce_sum_(diag, group)
-    pops = torch.empty(n, dtype=torch.float64, device=ens.dev)
-    scalars = torch.empty(3, dtype=torch.float64, device=ens.dev)
+    packed = torch.zeros(n + 4, dtype=torch.float64, device=ens.dev)
     need_joint = OBS_JOINT in config.observables if want_joint is None else want_joint
     joint = torch.empty(dim, dtype=torch.float64, device=ens.dev) if need_joint else None
-    ens.handle.observe_reduce(diag, float(config.realizations), pops, scalars, joint)
-    purity = None
+    ens.handle.observe_reduce(diag, float(config.realizations), packed[:n], packed[n:n + 3], joint)
     if OBS_PURITY in config.observables:
         states = sharding.gather_states(ens.states(), group)
-        out = torch.empty(1, dtype=torch.float64, device=ens.dev)
-        ens.handle.overlap_sumsq(states, states.shape[0], states, states.shape[0], out)
-        purity = float(out.item()) / float(config.realizations) ** 2
-    pops_h = pops.cpu().numpy()
-    sc = scalars.cpu().numpy()
-    joint_h = joint.cpu().numpy() if joint is not None else None
-    return pops_h, float(sc[2]), purity, joint_h, diag
+        ens.handle.overlap_sumsq(states, states.shape[0], states, states.shape[0], packed[n + 3:])
+    return PendingObservables(config, packed, diag, joint, n)
+
+
+def collect_observables(config, ens: EnsembleState, group=None, want_joint=None):
+    """Device reduction of one collection point -> (pops, pr, purity, joint, diag)."""
+    obs = collect_observables_async(config, ens, group, want_joint)
+    return obs.populations, obs.participation_ratio, obs.purity, obs.joint(), obs.diag_dev
 
 
 def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunReport:
@@ -488,9 +527,17 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
             if span > 0:
                 t0 = clock()
                 ens.evolve(previous, span)
+                t_ev = clock()
+            # the collection point is enqueued behind the segment; the single
+            # synchronisation below (statistics) covers both
+            t_obs0 = clock()
+            pending = collect_observables_async(config, ens, group)
+            t_obs1 = clock()
+            if span > 0:
                 local = ens.stats()
                 merged = sharding.merge_segment_stats(sharding.gather_objects(local, group))
-                profile.add(STAGE_EVOLUTION, clock() - t0, calls=config.realizations * span)
+                profile.add(STAGE_EVOLUTION, (t_ev - t0) + (clock() - t_obs1),
+                            calls=config.realizations * span)
                 # static noise: the Hamiltonian is generated on the fly, nothing to update
                 profile.add(STAGE_HAMILTONIAN, 0.0, calls=config.realizations * span)
                 if merged["failure"] is not None:
@@ -508,13 +555,15 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
                           for d, c, r, s in merged["events"]])
             previous = target
             with profile.stage(STAGE_DENSITY):
-                pops, pr, purity, joint, diag = collect_observables(config, ens, group)
+                profile.add(STAGE_DENSITY, t_obs1 - t_obs0, calls=0)
+                pops = pending.populations
+                joint = pending.joint() if OBS_JOINT in config.observables else None
                 time_tag = target * config.stepper.dt
-                rows = _observable_rows(config, pops, pr, purity, joint)
-                rho = DiagonalDensity(diag=(diag / config.realizations).cpu().numpy(),
-                                      dim=config.space.dim, sample_count=config.realizations,
-                                      time_tag=float(time_tag), purity=purity, populations=pops,
-                                      participation_ratio=pr)
+                rows = _observable_rows(config, pops, pending.participation_ratio, pending.purity, joint)
+                rho = DiagonalDensity(diag=None, dim=config.space.dim, sample_count=config.realizations,
+                                      time_tag=float(time_tag), purity=pending.purity, populations=pops,
+                                      participation_ratio=pending.participation_ratio,
+                                      device_diag=pending.diag_dev)
             snapshots += 1
             emit(sinks.observable_rows, rho.time_tag, rows)
             emit(sinks.density_snapshot, rho, target)

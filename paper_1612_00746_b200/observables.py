@@ -34,17 +34,30 @@ class PositionStats:
     wrapped: bool
 
 
-@dataclass
 class DiagonalDensity:
-    """diag(<rho>) with provenance; ``purity`` is set when it was requested."""
+    """diag(<rho>) with provenance; ``purity`` is set when it was requested.
 
-    diag: np.ndarray
-    dim: int
-    sample_count: int
-    time_tag: float
-    purity: float | None = None
-    populations: np.ndarray | None = None
-    participation_ratio: float | None = None
+    The diagonal may stay on the device (``device_diag``, the realization sum)
+    until it is first read, so sinks that drop snapshots cost no transfer.
+    """
+
+    def __init__(self, diag, dim, sample_count, time_tag, purity=None, populations=None,
+                 participation_ratio=None, device_diag=None):
+        self._diag = None if diag is None else np.asarray(diag, dtype=np.float64)
+        self._device_diag = device_diag
+        self.dim = int(dim)
+        self.sample_count = int(sample_count)
+        self.time_tag = float(time_tag)
+        self.purity = purity
+        self.populations = populations
+        self.participation_ratio = participation_ratio
+
+    @property
+    def diag(self) -> np.ndarray:
+        if self._diag is None:
+            self._diag = (self._device_diag / self.sample_count).cpu().numpy()
+            self._device_diag = None
+        return self._diag
 
     def diagonal(self) -> np.ndarray:
         return self.diag.astype(np.complex128)
