@@ -354,9 +354,7 @@ def ours(a):
     achieved = bytes_per_launch / (avg_launch_ms / 1000.0) / 1e9
     peak, peak_src = measured_peak_hbm()
     traffic = ncu_traffic()
-    kernel = "band_ws_kernel" if a.n > 64 else "resident_kernel"
-    if os.environ.get("CTQW_STREAM") == "tile" and a.n > 64:
-        kernel = "tile_step_kernel"
+    kernel = h.step_kernel()
     traffic_bytes = None
     if traffic and traffic.get("kernel") == kernel and a.n == 256 and a.m == 2:
         # ncu --set full capture (profiles/), per realization-step, scaled to this launch

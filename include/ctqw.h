@@ -193,6 +193,10 @@ int64_t ctqw_launch_count(ctqw_handle_t h);
 int ctqw_kernel_timing(ctqw_handle_t h, int32_t enable);
 int ctqw_kernel_time(ctqw_handle_t h, double *total_ms, int64_t *launches, void *stream);
 
+/* Name of the dominant kernel the last ctqw_evolve on this handle ran
+ * ("band4_kernel", "resident_kernel", ...; "" for the generic path). */
+const char *ctqw_step_kernel(ctqw_handle_t h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,7 +56,8 @@ struct ctqw_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int64_t timed_launches = 0;
-  int stream_kind = 0;  // 0 band (default), 1 tile (CTQW_STREAM=tile)
+  int stream_kind = 0;  // CTQW_STREAM: 0 auto (band4 > band2 > band > tile), 1 tile, 2 band, 3 band2, 4 band4
+  const char* stream_kernel = "";  // dominant kernel of the last ctqw_evolve
   std::string err;
 };
 
@@ -304,7 +305,13 @@ int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
   }
   long long nf = kNoFail;
   cudaMemcpy(h->fail, &nf, sizeof(nf), cudaMemcpyHostToDevice);
-  if (const char* sk = std::getenv("CTQW_STREAM")) h->stream_kind = std::strcmp(sk, "tile") == 0 ? 1 : 0;
+  if (const char* sk = std::getenv("CTQW_STREAM")) {
+    h->stream_kind = std::strcmp(sk, "tile") == 0    ? 1
+                     : std::strcmp(sk, "band") == 0  ? 2
+                     : std::strcmp(sk, "band2") == 0 ? 3
+                     : std::strcmp(sk, "band4") == 0 ? 4
+                                                     : 0;
+  }
   *out = h;
   return CTQW_OK;
 }
@@ -502,7 +509,9 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   double2* psi = (double2*)psi_dev;
   double2* work = (double2*)work_dev;
 
-  if (resident_supported(h->m, h->n, sc)) {
+  // a pinned streaming family (CTQW_STREAM) bypasses the resident path
+  if (h->stream_kind == 0 && resident_supported(h->m, h->n, sc)) {
+    h->stream_kernel = "resident_kernel";
     timing_event(h, s);
     CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step, n_steps,
                                 h->stats, h->events, h->fail, s));
@@ -512,13 +521,22 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
     return CTQW_OK;
   }
   if (!work) return fail_with(h, CTQW_ERR_CONFIG, "work buffer required");
-  // streaming m = 2 path: row-marching band kernel (default) or the v1 tile
-  // kernel (CTQW_STREAM=tile, kept for A/B measurements)
-  const bool use_band2 = band2_supported(h->m, h->n, sc, exact) && h->stream_kind != 1;
-  const bool use_band = !use_band2 && band_supported(h->m, h->n, sc) && h->stream_kind != 1;
-  const bool use_tile = !use_band2 && !use_band && tile_supported(h->m, h->n, sc);
-  if (use_band2 || use_band || use_tile) {
-    const int nparts = use_band2 ? band2_parts(h->n, sc, coef.site != nullptr, count)
+  // streaming m = 2 path: the four-column band kernel by default; the older
+  // band / band2 / tile kernels stay selectable for A/B measurements
+  // CTQW_STREAM pins one kernel family (A/B measurements, per-kernel parity
+  // tests); a pinned family that does not support the case falls through
+  // to the next one in auto order.
+  const int kind = h->stream_kind;
+  const bool use_band4 = (kind == 0 || kind == 4) && band4_supported(h->m, h->n, sc);
+  const bool use_band2 = !use_band4 && (kind == 0 || kind == 3 || kind == 4) &&
+                         band2_supported(h->m, h->n, sc, exact, kind == 3);
+  const bool use_band = !use_band4 && !use_band2 && kind != 1 && band_supported(h->m, h->n, sc);
+  const bool use_tile = !use_band4 && !use_band2 && !use_band && tile_supported(h->m, h->n, sc);
+  if (use_band4 || use_band2 || use_band || use_tile) {
+    h->stream_kernel = use_band4 ? "band4_kernel" : use_band2 ? "band2_kernel"
+                       : use_band ? "band_ws_kernel" : "tile_step_kernel";
+    const int nparts = use_band4 ? band4_parts(h->n)
+                       : use_band2 ? band2_parts(h->n, sc, coef.site != nullptr, count)
                        : use_band ? band_parts(h->n, sc, coef.site != nullptr, count)
                                   : tile_parts(h->n, sc);
     rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
@@ -528,7 +546,10 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       const double2* in = bufs[j & 1];
       double2* out = bufs[(j + 1) & 1];
       timing_event(h, s);
-      if (use_band2)
+      if (use_band4)
+        CUDA_TRY(h, launch_band4_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
+                                      h->fail, s));
+      else if (use_band2)
         CUDA_TRY(h, launch_band2_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
                                       h->fail, s));
       else if (use_band)
@@ -550,6 +571,7 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
     return CTQW_OK;
   }
   // generic path: in place on psi; work = term buffer A, library scratch B, C
+  h->stream_kernel = sc.backend == CTQW_BACKEND_TAYLOR ? "taylor_order_kernel" : "rk4_stage_kernel";
   rc = ensure_scratch(h, count * h->dim);
   if (rc) return rc;
   const int nparts = generic_parts(h->dim);
@@ -685,6 +707,8 @@ int ctqw_kernel_timing(ctqw_handle_t h, int32_t enable) {
   h->timed_launches = 0;
   return CTQW_OK;
 }
+
+const char* ctqw_step_kernel(ctqw_handle_t h) { return h ? h->stream_kernel : ""; }
 
 int ctqw_kernel_time(ctqw_handle_t h, double* total_ms, int64_t* launches, void* stream) {
   if (!h || !total_ms || !launches) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");

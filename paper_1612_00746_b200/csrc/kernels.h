@@ -67,8 +67,16 @@ cudaError_t launch_tile_step(const double2* psi_in, double2* psi_out, int64_t co
                              const Coef& coef, const StencilConst& k, const StepScalars& sc,
                              bool exact, const double* scl, double* partial,
                              const long long* fail, cudaStream_t s);
+// step_band4.cu (m = 2 row-marching kernel, four columns per thread, lag-1
+// pipeline, persistent row-block schedule; the default streaming path)
+bool band4_supported(int m, int n, const StepScalars& sc);
+int band4_parts(int n);
+cudaError_t launch_band4_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
+                              const Coef& coef, const StencilConst& k, const StepScalars& sc,
+                              bool exact, const double* scl, double* partial,
+                              const long long* fail, cudaStream_t s);
 // step_band2.cu (m = 2 row-marching kernel, two columns per thread)
-bool band2_supported(int m, int n, const StepScalars& sc, bool exact);
+bool band2_supported(int m, int n, const StepScalars& sc, bool exact, bool force);
 int band2_parts(int n, const StepScalars& sc, bool site, int64_t count);
 cudaError_t launch_band2_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
                               const Coef& coef, const StencilConst& k, const StepScalars& sc,

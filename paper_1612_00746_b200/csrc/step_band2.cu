@@ -469,20 +469,14 @@ int sm_count2() {
 
 }  // namespace
 
-bool band2_supported(int m, int n, const StepScalars& sc, bool exact) {
-  // Measured on B200: the two-column kernel wins for
-  // Taylor steps in FMA mode and for N = 512; the warp-specialised
-  // one-column kernel wins for exact-order Taylor at N <= 256, for RK4 (the
-  // pair kernel spills) and for haloed bands at N = 1024.
-  static int env = -1;
-  if (env < 0) {
-    const char* e = std::getenv("CTQW_BAND2");
-    env = e ? std::atoi(e) : -2;
-  }
-  if (env == 0) return false;
+bool band2_supported(int m, int n, const StepScalars& sc, bool exact, bool force) {
+  // Measured on B200: before the four-column kernel,
+  // the two-column kernel won for Taylor steps in FMA mode and for N = 512;
+  // the warp-specialised one-column kernel for exact-order Taylor at
+  // N <= 256, for RK4 (the pair kernel spills) and for haloed bands.
   const bool ok = m == 2 && n >= 16 && (sc.backend == 1 || (sc.order >= 1 && sc.order <= 4));
   if (!ok) return false;
-  if (env == 1) return true;
+  if (force) return true;
   return sc.backend == 0 && n <= 512 && (!exact || n > 256);
 }
 

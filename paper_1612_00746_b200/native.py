@@ -106,6 +106,7 @@ SIGNATURES = {
     "ctqw_launch_count": (ctypes.c_int64, [_P]),
     "ctqw_kernel_timing": (ctypes.c_int, [_P, _I32]),
     "ctqw_kernel_time": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
+    "ctqw_step_kernel": (ctypes.c_char_p, [_P]),
 }
 
 _lib = None
@@ -284,6 +285,10 @@ class Handle:
         n = _I64(0)
         self._check(self.lib.ctqw_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n), self.stream))
         return float(ms.value), int(n.value)
+
+    def step_kernel(self) -> str:
+        """Name of the dominant kernel the last evolve ran ('' = generic path)."""
+        return (self.lib.ctqw_step_kernel(self._h) or b"").decode()
 
     def overlap_sumsq(self, a, count_a: int, b, count_b: int, out):
         self._check(self.lib.ctqw_overlap_sumsq(self._h, _ptr(a), int(count_a), _ptr(b),

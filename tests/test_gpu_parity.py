@@ -380,3 +380,72 @@ def test_realization_independence_of_batching(pkg):
     h.bind(hop[2:5], site[2:5], 3, n)
     part, _ = run_evolve(h, psi0[2:5], 3, 12, stepper(dt=0.03))
     np.testing.assert_array_equal(full[2:5], part)
+
+
+# ---------------------------------------------------------------------------
+# every streaming kernel family on the same cases (CTQW_STREAM pins one)
+
+FAMILY_CASES = [CASES[4], CASES[6], CASES[8], CASES[10], CASES[11], CASES[12]]
+
+
+@pytest.mark.parametrize("family", ["band4", "band2", "band", "tile"])
+@pytest.mark.parametrize("case", FAMILY_CASES, ids=[f"n{c[1]}{c[3]}{c[4]}" for c in FAMILY_CASES])
+def test_stream_families_match_oracle(pkg, monkeypatch, family, case):
+    m, n, B, backend, order, dt, steps, target = case
+    monkeypatch.setenv("CTQW_STREAM", family)
+    h, st, _keep = device_case(m, n, B, target)
+    psi0 = np.tile(orc.product_state(m, n), (B, 1))
+    mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, order, dt))
+    ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, order)
+    assert_stats_match(stats, ostats)
+    if ostats.event_count == 0:
+        np.testing.assert_array_equal(mine, ref)
+    else:
+        assert np.abs(mine - ref).max() <= 1e-13
+
+
+BAND4_CASES = [
+    # (n, B, backend, order, dt, steps, target)
+    (1024, 1, "taylor", 4, 0.02, 3, "both"),   # 256-thread full row, compile-time N
+    (20, 4, "taylor", 4, 0.05, 20, "both"),    # runtime N, one norm block per row ring
+    (36, 3, "rk4", 4, 0.05, 15, "onsite"),     # ring rows padded (36 % 8 != 0)
+    (96, 300, "taylor", 4, 0.03, 4, "both"),   # persistent pieces cross realizations
+    (256, 40, "rk4", 4, 0.02, 3, "tunneling"), # compile-time N, RK4
+    (64, 5, "taylor", 3, 0.04, 6, "both"),     # order 3
+    (128, 3, "taylor", 2, 0.03, 8, "both"),    # order 2
+    (48, 3, "taylor", 1, 0.005, 8, "both"),    # order 1
+]
+
+
+@pytest.mark.parametrize("case", BAND4_CASES, ids=[f"n{c[0]}B{c[1]}{c[2]}{c[3]}" for c in BAND4_CASES])
+def test_band4_matches_oracle(pkg, monkeypatch, case):
+    n, B, backend, order, dt, steps, target = case
+    monkeypatch.setenv("CTQW_STREAM", "band4")
+    h, st, _keep = device_case(2, n, B, target)
+    psi0 = np.tile(orc.product_state(2, n), (B, 1))
+    mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, order, dt))
+    assert h.step_kernel() == "band4_kernel"
+    ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, order)
+    assert_stats_match(stats, ostats)
+    if ostats.event_count == 0:
+        np.testing.assert_array_equal(mine, ref)
+    else:
+        assert np.abs(mine - ref).max() <= 1e-13
+    # FMA mode stays within the north-star tolerance
+    fma, _ = run_evolve(h, psi0, B, steps, stepper(backend, order, dt, exact=False))
+    assert np.abs(fma - ref).max() <= 1e-12
+
+
+def test_band4_norm_partials_independent_of_batch(pkg, monkeypatch):
+    """Row-block norm partials: a realization's bits do not depend on how the
+    persistent schedule cut the batch (here 1 vs 500 realizations)."""
+    monkeypatch.setenv("CTQW_STREAM", "band4")
+    B, n = 500, 96
+    h, _, _keep = device_case(2, n, B, "both")
+    psi0 = np.tile(orc.product_state(2, n), (B, 1))
+    full, sf = run_evolve(h, psi0, B, 30, stepper(dt=0.05))
+    assert sf.corrections > 0  # renormalisation exercised
+    hop, site = _keep
+    h.bind(hop[137:138], site[137:138], 1, n)
+    one, _ = run_evolve(h, psi0[137:138], 1, 30, stepper(dt=0.05))
+    np.testing.assert_array_equal(full[137:138], one)
