@@ -46,8 +46,12 @@
 #include "ctqw_device.cuh"
 #include "kernels.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 namespace ctqw {
 
@@ -60,6 +64,7 @@ constexpr int kRB = 32;         // rows per norm block
 constexpr int kMaxThreads4 = 256;
 
 struct Band4Args {
+  CUtensorMap tmap;   // psi_in as [count*n rows][n/8 lines][16 doubles], 128B-swizzled boxes of one row
   const double2* psi_in;
   double2* psi_out;
   int n;
@@ -94,6 +99,37 @@ __device__ __forceinline__ void st256(double2* p, double2 a, double2 b) {
                : "memory");
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// One psi row (n complex = n/8 lines of 128 B) global -> shared through TMA,
+// 128B-swizzled: 16-byte chunk c lands at chunk c ^ ((c >> 3) & 7), which is
+// swz(c) because the destination slot is 1024-byte aligned.
+__device__ __forceinline__ void tma_row(uint32_t dst, const CUtensorMap* tm, int grow, uint32_t bar,
+                                        uint32_t bytes) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(tm), "r"(0), "r"(0), "r"(grow), "r"(bar)
+      : "memory");
+}
+
 struct Row4 {
   double2 c[kCols];
 };
@@ -104,7 +140,9 @@ struct Geo4 {
   int n_, npad_, rb_;
   __device__ __forceinline__ int n() const { return NN > 0 ? NN : n_; }
   __device__ __forceinline__ int np() const { return n() / kCols; }
-  __device__ __forceinline__ int npad() const { return NN > 0 ? ((NN + 7) & ~7) : npad_; }
+  // ring row stride in chunks: compile-time sizes use TMA rows, whose slots
+  // must be 1024-byte aligned (multiple of 64 chunks)
+  __device__ __forceinline__ int npad() const { return NN > 0 ? ((NN + 63) & ~63) : npad_; }
   __device__ __forceinline__ int rb() const { return NN > 0 ? (NN % kRB == 0 ? kRB : NN) : rb_; }
   __device__ __forceinline__ int wrap(int r) const { return r < 0 ? r + n() : (r >= n() ? r - n() : r); }
 };
@@ -115,10 +153,28 @@ struct T4 {
   int p, pl, pr;
   int off[kCols];     // swizzled ring offsets of own columns
   int offl, offr;     // swizzled ring offsets of columns 4p-1 and 4p+4
+  const double* colc; // smem column couplings: [q][NP] hop[4p+q] (q < 4), hop[4p-1] (q = 4), site[4p+q] (5..8)
+  int NP;
+};
+
+// Column couplings of the thread's four columns, re-read from shared memory
+// at every stencil application (holding them in registers spills).
+struct ColC {
   double hc[kCols];   // hop[x]      (particle 1 +move coupling)
   double hm0;         // hop[4p-1]   (particle 1 -move coupling of column 0)
   double sx[kCols];   // site[x]
 };
+
+template <bool SITE>
+__device__ __forceinline__ ColC load_colc(const T4& T) {
+  ColC c;
+#pragma unroll
+  for (int q = 0; q < kCols; ++q) c.hc[q] = T.colc[q * T.NP + T.p];
+  c.hm0 = T.colc[kCols * T.NP + T.p];
+#pragma unroll
+  for (int q = 0; q < kCols; ++q) c.sx[q] = SITE ? T.colc[(kCols + 1 + q) * T.NP + T.p] : 0.0;
+  return c;
+}
 
 struct Piece4 {
   const double2* src;
@@ -128,9 +184,11 @@ struct Piece4 {
   double s;
   bool scale;
   int pend;           // norm block awaiting its flush (-1 none)
+  int64_t grow0;      // TMA row coordinate of psi row 0 of this realization (r * n)
+  uint32_t* ph;       // per-slot mbarrier phase bits (TMA path)
 };
 
-extern __shared__ __align__(128) double2 smem4[];
+extern __shared__ __align__(1024) double2 smem4[];
 
 // Shared-memory layout (element offsets): ring [kRing4][npad], xl/xr
 // [NX][2][NP], hop2 [n], then doubles: site [n], red [64].
@@ -148,39 +206,47 @@ struct Lay4 {
     return reinterpret_cast<double*>(smem4 + hop2(g) + g.n());
   }
   __device__ __forceinline__ static double* red(const Geo4<NN>& g) { return site(g) + (SITE ? g.n() : 0); }
+  __device__ __forceinline__ static double* colc(const Geo4<NN>& g) { return red(g) + 64; }
+  __device__ __forceinline__ static uint64_t* bars(const Geo4<NN>& g) {
+    return reinterpret_cast<uint64_t*>(colc(g) + 9 * g.np());
+  }
 };
 
-template <int NN>
-__device__ __forceinline__ Row4 ring_row(const Geo4<NN>& g, const T4& T, int slot, double s, bool scale) {
+// SC: multiply by the pending rescale s (the CTA's realization had a norm
+// correction last step); s == 1.0 otherwise, so skipping is exact.
+template <bool SC, int NN>
+__device__ __forceinline__ Row4 ring_row(const Geo4<NN>& g, const T4& T, int slot, double s) {
   const double2* rowp = smem4 + slot * g.npad();
   Row4 v;
 #pragma unroll
   for (int q = 0; q < kCols; ++q) {
     v.c[q] = rowp[T.off[q]];
-    if (scale) v.c[q] = rmul(s, v.c[q]);
+    if (SC) v.c[q] = rmul(s, v.c[q]);
   }
   return v;
 }
 
 // (H z)(r, x) for the thread's four columns of row r: up = row r-1,
 // mid = row r, dn = row r+1, lf / rt = columns 4p-1 / 4p+4 of row r.
-template <bool EXACT, bool SITE>
+// DG: the diagonal carries the coincidence term (base[1] != base[0], U != 0).
+template <bool EXACT, bool SITE, bool DG>
 __device__ __forceinline__ void apply4(const T4& T, const StencilConst& K, int r, double2 hp,
                                        double srow, const Row4& up, const Row4& mid,
                                        const Row4& dn, double2 lf, double2 rt, double ci,
                                        Row4& out) {
   const int d = r - kCols * T.p;  // diagonal column offset within the thread's four
+  const ColC C = load_colc<SITE>(T);
 #pragma unroll
   for (int q = 0; q < kCols; ++q) {
-    double v0 = d == q ? K.base[1] : K.base[0];
-    if (SITE) v0 = __dadd_rn(v0, __dadd_rn(srow, T.sx[q]));  // base + (site[x0] + site[x1])
+    double v0 = (DG && d == q) ? K.base[1] : K.base[0];
+    if (SITE) v0 = __dadd_rn(v0, __dadd_rn(srow, C.sx[q]));  // base + (site[x0] + site[x1])
     const double2 l = q == 0 ? lf : mid.c[q - 1];
     const double2 rr = q == kCols - 1 ? rt : mid.c[q + 1];
-    const double hm = q == 0 ? T.hm0 : T.hc[q - 1];
+    const double hm = q == 0 ? C.hm0 : C.hc[q - 1];
     double2 h = rmul(v0, mid.c[q]);
     h = madd<EXACT>(h, hp.y, dn.c[q]);  // particle 0 +move: row r+1, hop[r]
     h = madd<EXACT>(h, hp.x, up.c[q]);  // particle 0 -move: row r-1, hop[r-1]
-    h = madd<EXACT>(h, T.hc[q], rr);    // particle 1 +move
+    h = madd<EXACT>(h, C.hc[q], rr);    // particle 1 +move
     h = madd<EXACT>(h, hm, l);          // particle 1 -move
     out.c[q] = times_i(ci, h);
   }
@@ -190,7 +256,6 @@ template <int NAPP>
 struct Regs4 {
   Row4 w[NAPP][3];  // w[k], k >= 1: stage-k output window (input of stage k+1); w[0] unused
   Row4 acc[3];      // running sums, slot = row mod 3 (relative)
-  Row4 psi;         // psi(j) (own columns, scaled), carried from the previous iteration
   Row4 up;          // psi(j-1): read by stage 1, reused by RK4 stage 2
   double nrm;
 };
@@ -220,7 +285,7 @@ __device__ __forceinline__ void band4_store(const Geo4<NN>& g, const T4& T, Piec
 // Stage K (2..NAPP) of iteration j: row j-K+1 from window K-1 (rows j-K ..
 // j-K+2, slot(y) = (y - j0) mod 3) and the neighbour columns stage K-1
 // published last iteration.
-template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, int PH, int K>
+template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, bool DG, int PH, int K>
 __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& g, const T4& T, Piece4& P,
                                             Regs4<NAPP>& R, int i, int j) {
   using L = Lay4<NN, NAPP, SITE>;
@@ -234,7 +299,7 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   const double2 rt = smem4[L::xl(g, K - 2, buf ^ 1) + T.pr];
   const double ci = RK4 ? a.ci[0] : a.ci[K - 1];
   Row4 tk;
-  apply4<EXACT, SITE>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0, R.w[K - 1][sm],
+  apply4<EXACT, SITE, DG>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0, R.w[K - 1][sm],
                       R.w[K - 1][s0], R.w[K - 1][sp], lf, rt, ci, tk);
   if constexpr (K == NAPP) {
     const int jo = j - K + 1;
@@ -246,11 +311,12 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   } else {
     Row4 nk;
     if (RK4) {
-      if (K == 2) {  // arg = 0.5*k2 + psi(j-1)
+      if (K == 2) {  // arg = 0.5*k2 + psi(j-1) (re-read: keeping it from stage 1 spills)
+        const Row4 pm = ring_row<SC>(g, T, i & (kRing4 - 1), P.s);
 #pragma unroll
-        for (int q = 0; q < kCols; ++q) nk.c[q] = cadd(rmul(0.5, tk.c[q]), R.up.c[q]);
+        for (int q = 0; q < kCols; ++q) nk.c[q] = cadd(rmul(0.5, tk.c[q]), pm.c[q]);
       } else {  // K == 3: arg = k3 + psi(j-2)
-        const Row4 pm = ring_row(g, T, (i - 1) & (kRing4 - 1), P.s, P.scale);
+        const Row4 pm = ring_row<SC>(g, T, (i - 1) & (kRing4 - 1), P.s);
 #pragma unroll
         for (int q = 0; q < kCols; ++q) nk.c[q] = cadd(tk.c[q], pm.c[q]);
       }
@@ -267,19 +333,35 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   }
 }
 
+// Ring slot rho & 7 <- psi row j0 - 1 + rho.  Compile-time sizes: one TMA
+// box issued by thread 0, completion on the slot's mbarrier.  Runtime sizes:
+// every thread cp.asyncs n/NP 16-byte chunks (lane-contiguous in global
+// memory, XOR-swizzled in shared memory).
 template <int NN>
-__device__ __forceinline__ void band4_load_row(const Geo4<NN>& g, const T4& T, const Piece4& P, int rho) {
+__device__ __forceinline__ void band4_load_row(const Band4Args& a, const Geo4<NN>& g, const T4& T,
+                                               const Piece4& P, int rho, uint32_t bars) {
   const int y = g.wrap(g.wrap(P.j0 - 1 + rho));
-  double2* slot = smem4 + (rho & (kRing4 - 1)) * g.npad();
-  const double2* src = P.src + (int64_t)y * g.n();
-  if (NN > 0) {
-#pragma unroll
-    for (int c0 = 0; c0 < (NN > 0 ? NN : 1); c0 += (NN > 0 ? NN / kCols : 1)) {
-      const int c = c0 + T.p;
-      cpa16(slot + swz(c), src + c);
-    }
+  const int slot = rho & (kRing4 - 1);
+  if constexpr (NN > 0) {
+    if (T.p == 0)
+      tma_row(smem_u32(smem4 + slot * g.npad()), &a.tmap, (int)(P.grow0 + y), bars + 8 * slot,
+              (uint32_t)(NN * sizeof(double2)));
   } else {
-    for (int c = T.p; c < g.n(); c += g.np()) cpa16(slot + swz(c), src + c);
+    double2* dst = smem4 + slot * g.npad();
+    const double2* src = P.src + (int64_t)y * g.n();
+    for (int c = T.p; c < g.n(); c += g.np()) cpa16(dst + swz(c), src + c);
+  }
+}
+
+// Wait until ring row rho has landed (TMA path: the slot's mbarrier phase).
+template <int NN>
+__device__ __forceinline__ void band4_wait_row(Piece4& P, int rho, uint32_t bars) {
+  if constexpr (NN > 0) {
+    if (rho <= P.last_rho) {
+      const int slot = rho & (kRing4 - 1);
+      mbar_wait(bars + 8 * slot, (*P.ph >> slot) & 1u);
+      *P.ph ^= 1u << slot;
+    }
   }
 }
 
@@ -298,51 +380,54 @@ __device__ __forceinline__ void band4_flush(const Geo4<NN>& g, const T4& T, Piec
 // One pipeline iteration.  PH = (iteration index) mod 3 selects register
 // slots; i = iteration index (j = j0 + i); rho(y) = y - (j0 - 1) is a row's
 // ring index.
-template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, int PH>
+template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, bool DG, int PH>
 __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g, const T4& T, Piece4& P,
-                                           Regs4<NAPP>& R, int i) {
+                                           Regs4<NAPP>& R, int i, uint32_t bars) {
   using L = Lay4<NN, NAPP, SITE>;
   const int j = P.j0 + i;
   // rho = i + 2 (psi(j+1)) must have landed; the barrier also publishes the
   // neighbour columns of the last iteration and retires its ring reads.
-  cpa_wait<kPref4 - 2>();
+  if constexpr (NN > 0) {
+    band4_wait_row<NN>(P, i + 2, bars);
+  } else {
+    cpa_wait<kPref4 - 2>();
+  }
   __syncthreads();
   band4_flush<NN, NAPP, SITE>(g, T, P);
-  if (i + kPref4 + 1 <= P.last_rho) band4_load_row(g, T, P, i + kPref4 + 1);
-  cpa_commit();
+  if (i + kPref4 + 1 <= P.last_rho) band4_load_row(a, g, T, P, i + kPref4 + 1, bars);
+  if constexpr (NN == 0) cpa_commit();
   const int buf = i & 1;
   constexpr double c16 = 1.0 / 6.0;
   constexpr int SM1 = (PH + 2) % 3;  // slot of row j-1
 
-  // ---- stage 1: row j.  psi(j-1) and psi(j+1) come from the ring, psi(j)
-  // was carried in registers from the previous iteration.
+  // ---- stage 1: row j; psi(j-1), psi(j), psi(j+1) come from the ring.
   const int r = g.wrap(j);
-  R.up = ring_row(g, T, i & (kRing4 - 1), P.s, P.scale);
-  const Row4 dn = ring_row(g, T, (i + 2) & (kRing4 - 1), P.s, P.scale);
+  R.up = ring_row<SC>(g, T, i & (kRing4 - 1), P.s);
+  const Row4 psi = ring_row<SC>(g, T, (i + 1) & (kRing4 - 1), P.s);  // psi(j): re-read, not carried
+  const Row4 dn = ring_row<SC>(g, T, (i + 2) & (kRing4 - 1), P.s);
   const double2* rowj = smem4 + ((i + 1) & (kRing4 - 1)) * g.npad();
   double2 lf = rowj[T.offl], rt = rowj[T.offr];
-  if (P.scale) {
+  if (SC) {
     lf = rmul(P.s, lf);
     rt = rmul(P.s, rt);
   }
   Row4 t;
-  apply4<EXACT, SITE>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, R.psi, dn, lf, rt,
+  apply4<EXACT, SITE, DG>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, psi, dn, lf, rt,
                       a.ci[0], t);
   if constexpr (NAPP == 1) {
     Row4 o;
 #pragma unroll
-    for (int q = 0; q < kCols; ++q) o.c[q] = cadd(R.psi.c[q], t.c[q]);
+    for (int q = 0; q < kCols; ++q) o.c[q] = cadd(psi.c[q], t.c[q]);
     if (j >= P.ya && j < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, r, o, R.nrm);
-    R.psi = dn;
   } else {
     Row4 nt;
     if (RK4) {
 #pragma unroll
-      for (int q = 0; q < kCols; ++q) nt.c[q] = cadd(rmul(0.5, t.c[q]), R.psi.c[q]);
+      for (int q = 0; q < kCols; ++q) nt.c[q] = cadd(rmul(0.5, t.c[q]), psi.c[q]);
       // acc(j) = psi(j) + k1/6; slot PH still holds acc(j-3) until the last
       // stage has consumed it, so the row waits in `t`.
 #pragma unroll
-      for (int q = 0; q < kCols; ++q) t.c[q] = cadd(R.psi.c[q], rmul(c16, t.c[q]));
+      for (int q = 0; q < kCols; ++q) t.c[q] = cadd(psi.c[q], rmul(c16, t.c[q]));
     } else {
       // acc(j-1) = psi(j-1) + t1(j-1): both are at hand (psi(j-1) was just
       // read, t1(j-1) is window 1), and stage 2 below is its first update.
@@ -351,13 +436,23 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
       nt = t;
     }
     R.w[1][PH] = nt;
-    R.psi = dn;
     smem4[L::xl(g, 0, buf) + T.p] = nt.c[0];
     smem4[L::xr(g, 0, buf) + T.p] = nt.c[kCols - 1];
-    if constexpr (NAPP >= 2) band4_stage<NN, NAPP, RK4, SITE, EXACT, PH, 2>(a, g, T, P, R, i, j);
-    if constexpr (NAPP >= 3) band4_stage<NN, NAPP, RK4, SITE, EXACT, PH, 3>(a, g, T, P, R, i, j);
-    if constexpr (NAPP >= 4) band4_stage<NN, NAPP, RK4, SITE, EXACT, PH, 4>(a, g, T, P, R, i, j);
+    if constexpr (NAPP >= 2) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 2>(a, g, T, P, R, i, j);
+    if constexpr (NAPP >= 3) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 3>(a, g, T, P, R, i, j);
+    if constexpr (NAPP >= 4) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 4>(a, g, T, P, R, i, j);
     if (RK4) R.acc[PH] = t;
+  }
+}
+
+template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, bool DG>
+__device__ __forceinline__ void band4_loop(const Band4Args& a, const Geo4<NN>& g, const T4& T, Piece4& P,
+                                           Regs4<NAPP>& R, int iters, uint32_t bars) {
+#pragma unroll 1
+  for (int i = 0; i < iters; i += 3) {
+    band4_iter<NN, NAPP, RK4, SITE, EXACT, SC, DG, 0>(a, g, T, P, R, i, bars);
+    band4_iter<NN, NAPP, RK4, SITE, EXACT, SC, DG, 1>(a, g, T, P, R, i + 1, bars);
+    band4_iter<NN, NAPP, RK4, SITE, EXACT, SC, DG, 2>(a, g, T, P, R, i + 2, bars);
   }
 }
 
@@ -382,6 +477,18 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
   for (int q = 0; q < kCols; ++q) T.off[q] = swz(kCols * p + q);
   T.offl = swz(g.wrap(kCols * p - 1));
   T.offr = swz(g.wrap(kCols * p + kCols));
+  T.colc = L::colc(g);
+  T.NP = NP;
+
+  // TMA rows are 128B-swizzled relative to 1024-byte boundaries
+  if (NN > 0 && (smem_u32(smem4) & 1023u) != 0) __trap();
+  // TMA ring barriers (one per slot) live after the column table
+  uint32_t ph_bits = 0;
+  const uint32_t bars = smem_u32(L::bars(g));
+  if (NN > 0 && p == 0) {
+    for (int q = 0; q < kRing4; ++q) mbar_init(bars + 8 * q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
 
   // this CTA's contiguous run of norm blocks
   const int64_t G = gridDim.x;
@@ -405,28 +512,38 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
       hop2[y] = make_double2(hop[y == 0 ? n - 1 : y - 1], hop[y]);
       if (SITE) site[y] = sg[y];
     }
+    {
+      double* cc = L::colc(g);
 #pragma unroll
-    for (int q = 0; q < kCols; ++q) {
-      T.hc[q] = hop[kCols * p + q];
-      T.sx[q] = SITE ? sg[kCols * p + q] : 0.0;
+      for (int q = 0; q < kCols; ++q) {
+        cc[q * NP + p] = hop[kCols * p + q];
+        if (SITE) cc[(kCols + 1 + q) * NP + p] = sg[kCols * p + q];
+      }
+      cc[kCols * NP + p] = hop[g.wrap(kCols * p - 1)];
     }
-    T.hm0 = hop[g.wrap(kCols * p - 1)];
     P.s = a.scl ? a.scl[r] : 1.0;
     P.scale = P.s != 1.0;
     P.src = a.psi_in + r * dim;
     P.dst = a.psi_out + r * dim;
     P.part = a.partial + r * nblk;
     P.pend = -1;
+    P.grow0 = r * n;
+    P.ph = &ph_bits;
     P.j0 = P.ya - NAPP + 1;                    // first iteration's stage-1 row
     const int iters = (P.yb - P.ya) + 2 * (NAPP - 1);
     P.last_rho = iters + 1;                    // psi rows j0-1 .. j0+iters
     // prologue: rows rho = 0 .. kPref4 (one commit group each)
 #pragma unroll
     for (int rho = 0; rho <= kPref4; ++rho) {
-      if (rho <= P.last_rho) band4_load_row(g, T, P, rho);
-      cpa_commit();
+      if (rho <= P.last_rho) band4_load_row(a, g, T, P, rho, bars);
+      if constexpr (NN == 0) cpa_commit();
     }
-    cpa_wait<kPref4 - 1>();  // rho 0, 1 landed
+    if constexpr (NN > 0) {
+      band4_wait_row<NN>(P, 0, bars);
+      band4_wait_row<NN>(P, 1, bars);
+    } else {
+      cpa_wait<kPref4 - 1>();  // rho 0, 1 landed
+    }
     __syncthreads();
     Regs4<NAPP> R;
 #pragma unroll
@@ -440,14 +557,13 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
 #pragma unroll
       for (int q = 0; q < kCols; ++q) R.acc[w].c[q] = make_double2(0.0, 0.0);
     R.nrm = 0.0;
-    R.psi = ring_row(g, T, 1, P.s, P.scale);  // psi(j0)
-#pragma unroll 1
-    for (int i = 0; i < iters; i += 3) {
-      band4_iter<NN, NAPP, RK4, SITE, EXACT, 0>(a, g, T, P, R, i);
-      band4_iter<NN, NAPP, RK4, SITE, EXACT, 1>(a, g, T, P, R, i + 1);
-      band4_iter<NN, NAPP, RK4, SITE, EXACT, 2>(a, g, T, P, R, i + 2);
+    if constexpr (NN > 0) {  // compile-time sizes: no rescale multiplies unless needed
+      if (P.scale) band4_loop<NN, NAPP, RK4, SITE, EXACT, true, true>(a, g, T, P, R, iters, bars);
+      else band4_loop<NN, NAPP, RK4, SITE, EXACT, false, true>(a, g, T, P, R, iters, bars);
+    } else {
+      band4_loop<NN, NAPP, RK4, SITE, EXACT, true, true>(a, g, T, P, R, iters, bars);
     }
-    cpa_wait<0>();
+    if constexpr (NN == 0) cpa_wait<0>();
     __syncthreads();
     band4_flush<NN, NAPP, SITE>(g, T, P);
   }
@@ -477,8 +593,33 @@ Band4Plan plan_band4(int n, int napp, bool site, int64_t count) {
   p.nblk = n / p.rb;
   const int nx = napp > 1 ? napp - 1 : 1;
   p.smem = (size_t)kRing4 * p.npad * sizeof(double2) + (size_t)nx * 4 * p.threads * sizeof(double2) +
-           (size_t)n * sizeof(double2) + (size_t)((site ? n : 0) + 64) * sizeof(double);
+           (size_t)n * sizeof(double2) + (size_t)((site ? n : 0) + 64 + 9 * p.threads) * sizeof(double) +
+           kRing4 * sizeof(uint64_t);
   return p;
+}
+
+// TMA descriptor of the input state stack: rows of n complex128 viewed as
+// n/8 lines of 16 doubles (128 B), one box = one row, 128B swizzle.
+cudaError_t encode_rows_map(CUtensorMap* map, const double2* base, int n, int64_t count) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!encode) return cudaErrorNotSupported;
+  if (n % 64 != 0 || n / 8 > 256 || count * n > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const cuuint64_t dims[3] = {16, (cuuint64_t)(n / 8), (cuuint64_t)(count * n)};
+  const cuuint64_t strides[2] = {128, (cuuint64_t)n * sizeof(double2)};
+  const cuuint32_t box[3] = {16, (cuuint32_t)(n / 8), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(base), dims, strides,
+                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, int NN>
@@ -497,7 +638,14 @@ cudaError_t launch_b4(const Band4Args& args, Band4Plan p, cudaStream_t s) {
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int64_t slots = (int64_t)occ * sm_count4();
   const int64_t grid = std::min<int64_t>(slots, args.count * p.nblk);
-  kern<<<(unsigned)grid, p.threads, p.smem, s>>>(args);
+  if constexpr (NN > 0) {
+    Band4Args a = args;
+    e = encode_rows_map(&a.tmap, a.psi_in, NN, a.count);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, p.threads, p.smem, s>>>(a);
+  } else {
+    kern<<<(unsigned)grid, p.threads, p.smem, s>>>(args);
+  }
   return cudaGetLastError();
 }
 
@@ -554,6 +702,9 @@ cudaError_t launch_band4_step(const double2* psi_in, double2* psi_out, int64_t c
   a.partial = partial;
   a.fail = fail;
   if (count == 0) return cudaSuccess;
+#ifdef B4_ONLY  // register-pressure experiments: one instantiation
+  return launch_b4<4, false, false, true, 256>(a, p, s);
+#else
   if (sc.backend == 1) return launch_b4_n<4, true>(a, p, site, exact, s);
   switch (napp) {
     case 1: return launch_b4_n<1, false>(a, p, site, exact, s);
@@ -562,6 +713,7 @@ cudaError_t launch_band4_step(const double2* psi_in, double2* psi_out, int64_t c
     case 4: return launch_b4_n<4, false>(a, p, site, exact, s);
     default: return cudaErrorInvalidValue;
   }
+#endif
 }
 
 }  // namespace ctqw

@@ -4,9 +4,10 @@ set -u
 TAG=${1:-q}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_K:-} > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_K:+-k "$PYTEST_K"} > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 tail -25 $OUT/pytest_gpu.log
-for args in "" "--fma" "--backend rk4" "--n 512" "--n 1024 --realizations 250" "--n 512 --fma" "--n 1024 --realizations 250 --fma"; do
+IFS=';' read -ra CASES <<< "${BENCH_CASES:-;--fma;--backend rk4;--n 512;--n 1024 --realizations 250;--n 512 --fma;--n 1024 --realizations 250 --fma}"
+for args in "${CASES[@]}"; do
   timeout 300 python bench.py --no-e2e --no-cpu --steps 50 --warmup 3 $args 2>>$OUT/bench.err | python -c "
 import json,sys
 for l in sys.stdin:
