@@ -56,7 +56,7 @@ struct ctqw_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int64_t timed_launches = 0;
-  int stream_kind = 0;  // CTQW_STREAM: 0 auto (band4 > band2 > band > tile), 1 tile, 2 band, 3 band2, 4 band4
+  int stream_kind = 0;  // CTQW_STREAM: 0 auto, 1 tile, 2 band, 3 band2, 4 band4, 5 plane3, 6 generic
   const char* stream_kernel = "";  // dominant kernel of the last ctqw_evolve
   std::string err;
 };
@@ -310,6 +310,8 @@ int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
                      : std::strcmp(sk, "band") == 0  ? 2
                      : std::strcmp(sk, "band2") == 0 ? 3
                      : std::strcmp(sk, "band4") == 0 ? 4
+                     : std::strcmp(sk, "plane3") == 0 ? 5
+                     : std::strcmp(sk, "generic") == 0 ? 6
                                                      : 0;
   }
   *out = h;
@@ -531,14 +533,16 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   // kernel for full-row N <= 512 (band4's RK4 carries one more row and spills)
   const bool rk4_ws = kind == 0 && sc.backend == CTQW_BACKEND_RK4 && exact && h->n % 32 == 0 && h->n <= 512;
   const bool use_band4 = (kind == 0 || kind == 4) && !rk4_ws && band4_supported(h->m, h->n, sc);
+  const bool use_plane3 = (kind == 0 || kind == 5) && plane3_supported(h->m, h->n, sc);
   const bool use_band2 = !use_band4 && (kind == 0 || kind == 3 || kind == 4) &&
                          band2_supported(h->m, h->n, sc, exact, kind == 3);
-  const bool use_band = !use_band4 && !use_band2 && kind != 1 && band_supported(h->m, h->n, sc);
-  const bool use_tile = !use_band4 && !use_band2 && !use_band && tile_supported(h->m, h->n, sc);
-  if (use_band4 || use_band2 || use_band || use_tile) {
-    h->stream_kernel = use_band4 ? "band4_kernel" : use_band2 ? "band2_kernel"
+  const bool use_band = !use_band4 && !use_band2 && kind != 1 && kind < 5 && band_supported(h->m, h->n, sc);
+  const bool use_tile = !use_band4 && !use_band2 && !use_band && kind < 5 && tile_supported(h->m, h->n, sc);
+  if (use_plane3 || use_band4 || use_band2 || use_band || use_tile) {
+    h->stream_kernel = use_plane3 ? "plane3_kernel" : use_band4 ? "band4_kernel" : use_band2 ? "band2_kernel"
                        : use_band ? "band_ws_kernel" : "tile_step_kernel";
-    const int nparts = use_band4 ? band4_parts(h->n)
+    const int nparts = use_plane3 ? plane3_parts()
+                       : use_band4 ? band4_parts(h->n)
                        : use_band2 ? band2_parts(h->n, sc, coef.site != nullptr, count)
                        : use_band ? band_parts(h->n, sc, coef.site != nullptr, count)
                                   : tile_parts(h->n, sc);
@@ -549,7 +553,9 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       const double2* in = bufs[j & 1];
       double2* out = bufs[(j + 1) & 1];
       timing_event(h, s);
-      if (use_band4)
+      if (use_plane3)
+        CUDA_TRY(h, launch_plane3_step(in, out, count, coef, h->k, sc, exact, h->scl, h->partial, h->fail, s));
+      else if (use_band4)
         CUDA_TRY(h, launch_band4_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
                                       h->fail, s));
       else if (use_band2)

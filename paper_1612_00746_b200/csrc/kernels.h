@@ -67,6 +67,13 @@ cudaError_t launch_tile_step(const double2* psi_in, double2* psi_out, int64_t co
                              const Coef& coef, const StencilConst& k, const StepScalars& sc,
                              bool exact, const double* scl, double* partial,
                              const long long* fail, cudaStream_t s);
+// step_plane3.cu (m = 3, N = 128: one 16-CTA cluster per realization, DSMEM
+// plane exchange, TMA plane ring)
+bool plane3_supported(int m, int n, const StepScalars& sc);
+int plane3_parts();
+cudaError_t launch_plane3_step(const double2* psi_in, double2* psi_out, int64_t count, const Coef& coef,
+                               const StencilConst& k, const StepScalars& sc, bool exact, const double* scl,
+                               double* partial, const long long* fail, cudaStream_t s);
 // step_band4.cu (m = 2 row-marching kernel, four columns per thread, lag-1
 // pipeline, persistent row-block schedule; the default streaming path)
 bool band4_supported(int m, int n, const StepScalars& sc);

@@ -1,0 +1,580 @@
+// Plane-marching streaming step kernel for m = 3 particles on an N = 128 ring
+// (joint dimension 2^21, BASELINE configs[4]).  One thread-block cluster of
+// 16 CTAs owns one realization; the cluster marches once down the 128 x0
+// planes per time step, every CTA holding an 8-row x1 band of each plane
+// (128 x2 columns), so a plane of 16384 amplitudes lives in the cluster's
+// distributed shared memory and registers.
+//
+// Pipeline (as step_band4.cu, with planes for rows): at iteration j stage k
+// computes plane j-k+1 from the three-plane register window of stage k-1's
+// output (own amplitudes) plus the in-plane neighbours of plane j-k+1 that
+// stage k-1 published one iteration earlier.  In-plane neighbours along x2
+// and inside the band along x1 come from the CTA's shared memory; the two x1
+// rows across the band edges come from the neighbouring CTAs' shared memory
+// (DSMEM).  One cluster barrier per plane replaces __syncthreads.
+//
+// Threads: 256 per CTA, thread (u, v) owns the 2x2 block x1 = 8c + 2u + {0,1},
+// x2 = 2v + {0,1}.  psi planes arrive by TMA (ten 2 KB rows per plane: the
+// band plus one halo row on each side, so stage 1 needs no DSMEM), 128B
+// swizzled, into a 6-plane ring with one mbarrier per slot.
+//
+// Arithmetic is the reference's (hamiltonian.py:205-222): diagonal
+// base[#coincident pairs] + ((site[x0] + site[x1]) + site[x2]), then for each
+// particle p = 0, 1, 2 the +move and the -move; Taylor terms summed in order,
+// RK4 stage arithmetic (propagators.py:185-193, 213-240).  EXACT rounds
+// every product and sum separately (bit-identical to the reference between
+// renormalisations).
+#include "ctqw_device.cuh"
+#include "kernels.h"
+
+#include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+namespace cg = cooperative_groups;
+
+namespace ctqw {
+
+namespace {
+
+constexpr int kN3 = 128;             // lattice sites
+constexpr int kCl = 16;              // CTAs per cluster (x1 bands)
+constexpr int kBand = kN3 / kCl;     // x1 rows per CTA
+constexpr int kTR = kBand + 2;       // ring rows per plane (band + x1 halo)
+constexpr int kRing3 = 6;            // psi planes resident
+constexpr int kPref3 = 3;            // planes requested ahead of the one consumed
+constexpr int kThreads3 = 256;       // 4 x1 pairs x 64 x2 pairs
+constexpr int kPB = 16;              // planes per norm block
+constexpr int kNblk3 = kN3 / kPB;    // norm blocks per realization per CTA
+constexpr int kRowB = kN3 * 16;      // bytes per x1 row (128 complex)
+constexpr int kPlaneB = kTR * kRowB; // ring bytes per plane
+
+struct Plane3Args {
+  CUtensorMap tmap;  // psi_in: (16 doubles, 16 lines, x1, count*N planes), box = one x1 row
+  double2* psi_out;
+  int64_t count;
+  Coef coef;
+  StencilConst k;
+  double ci[4];
+  const double* scl;
+  double* partial;
+  const long long* fail;
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int swz3(int c) { return c ^ ((c >> 3) & 7); }
+__device__ __forceinline__ int wrap3(int r) { return r & (kN3 - 1); }
+
+__device__ __forceinline__ void mbar_wait3(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void st256b(double2* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+               : "memory");
+}
+
+// the thread's 2x2 block: index q = 2a + b, x1 offset a, x2 offset b
+struct Quad {
+  double2 c[4];
+};
+
+// Shared memory (byte offsets from smem3): ring [kRing3][kTR][128] chunks;
+// exchange [3 stages][2 parity][kBand][128] chunks; hop2 [N] (hop[y-1],
+// hop[y]); site [N]; red [8] per-warp norm partials; mbarriers [kRing3].
+extern __shared__ __align__(1024) double2 smem3[];
+constexpr int kXOff = kRing3 * kTR * kN3;        // exchange, in double2 units
+constexpr int kXStage = 2 * kBand * kN3;
+constexpr int kHopOff = kXOff + 3 * kXStage;
+constexpr int kSiteOff = kHopOff + kN3;          // doubles follow, in double2 units of the base
+constexpr size_t kSmem3 = (size_t)(kSiteOff) * 16 + (size_t)kN3 * 8 + 16 * 8 + kRing3 * 8;
+
+__device__ __forceinline__ double* site_tab() { return reinterpret_cast<double*>(smem3 + kSiteOff); }
+__device__ __forceinline__ double* red_tab() { return site_tab() + kN3; }
+__device__ __forceinline__ uint32_t bar_addr(int slot) { return s_u32(red_tab() + 16) + 8 * slot; }
+
+struct T3 {
+  int u, v, c;          // x1 pair, x2 pair, cluster rank (x1 band)
+  int x1a, x2a;         // first owned x1 / x2
+  double h1[3];         // hop[x1a-1], hop[x1a], hop[x1a+1]
+  double h2[3];         // hop[x2a-1], hop[x2a], hop[x2a+1]
+  double s1[2], s2[2];  // site[x1a + a], site[x2a + b]
+  const double2* up_nb;   // x1 row above the band (DSMEM of rank c-1) for u == 0: exchange base
+  const double2* dn_nb;   // x1 row below the band (DSMEM of rank c+1) for u == 3
+};
+
+struct Piece3 {
+  double2* dst;
+  double* part;
+  int64_t g0;  // plane coordinate of x0 = 0 for this realization (r * N)
+  int j0, ya, yb, last_rho;
+  double s;
+  bool scale;
+  int pend;
+  uint32_t* ph;
+};
+
+template <int NAPP>
+struct Regs3 {
+  Quad w[NAPP][3];
+  Quad acc[3];
+  Quad up;
+  double nrm;
+};
+
+// ring element (row in the 10-row plane tile, x2 column)
+__device__ __forceinline__ double2 ring_at(int slot, int row, int col) {
+  return smem3[(slot * kTR + row) * kN3 + swz3(col)];
+}
+
+template <bool SC>
+__device__ __forceinline__ Quad ring_quad(const T3& T, int slot, double s) {
+  Quad v;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v.c[q] = ring_at(slot, 1 + 2 * T.u + (q >> 1), 2 * T.v + (q & 1));
+    if (SC) v.c[q] = rmul(s, v.c[q]);
+  }
+  return v;
+}
+
+// In-plane neighbours of the thread's block: x1m[b] (row x1a-1), x1p[b]
+// (row x1a+2), x2m[a] (column x2a-1), x2p[a] (column x2a+2).
+struct Nb {
+  double2 x1m[2], x1p[2], x2m[2], x2p[2];
+};
+
+template <bool SC>
+__device__ __forceinline__ Nb ring_nb(const T3& T, int slot, double s) {
+  Nb nb;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    nb.x1m[t] = ring_at(slot, 2 * T.u, 2 * T.v + t);
+    nb.x1p[t] = ring_at(slot, 2 * T.u + 3, 2 * T.v + t);
+    nb.x2m[t] = ring_at(slot, 1 + 2 * T.u + t, wrap3(2 * T.v - 1));
+    nb.x2p[t] = ring_at(slot, 1 + 2 * T.u + t, wrap3(2 * T.v + 2));
+    if (SC) {
+      nb.x1m[t] = rmul(s, nb.x1m[t]);
+      nb.x1p[t] = rmul(s, nb.x1p[t]);
+      nb.x2m[t] = rmul(s, nb.x2m[t]);
+      nb.x2p[t] = rmul(s, nb.x2p[t]);
+    }
+  }
+  return nb;
+}
+
+// exchange element of stage k (0-based output index), parity buf
+__device__ __forceinline__ int xoff(int k, int buf, int row, int col) {
+  return kXOff + k * kXStage + (buf * kBand + row) * kN3 + swz3(col);
+}
+
+__device__ __forceinline__ Nb xch_nb(const T3& T, int k, int buf) {
+  Nb nb;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    nb.x2m[t] = smem3[xoff(k, buf, 2 * T.u + t, wrap3(2 * T.v - 1))];
+    nb.x2p[t] = smem3[xoff(k, buf, 2 * T.u + t, wrap3(2 * T.v + 2))];
+    const int cm = 2 * T.v + t;
+    // rows across the band edge live in the neighbouring CTA (DSMEM);
+    // u is warp-uniform, so these branches do not diverge
+    if (T.u > 0) nb.x1m[t] = smem3[xoff(k, buf, 2 * T.u - 1, cm)];
+    else nb.x1m[t] = T.up_nb[xoff(k, buf, kBand - 1, cm)];
+    if (T.u < 3) nb.x1p[t] = smem3[xoff(k, buf, 2 * T.u + 2, cm)];
+    else nb.x1p[t] = T.dn_nb[xoff(k, buf, 0, cm)];
+  }
+  return nb;
+}
+
+__device__ __forceinline__ void xch_put(const T3& T, int k, int buf, const Quad& v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) smem3[xoff(k, buf, 2 * T.u + (q >> 1), 2 * T.v + (q & 1))] = v.c[q];
+}
+
+// (H z) on the block at plane r: up / mid / dn = planes r-1, r, r+1.
+template <bool EXACT, bool SITE>
+__device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
+                                       const Quad& dn, const Nb& nb, double ci, Quad& out) {
+  const double2 h0 = smem3[kHopOff + r];  // (hop[r-1], hop[r])
+  const double s0 = SITE ? site_tab()[r] : 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int a = q >> 1, b = q & 1;
+    const int x1 = T.x1a + a, x2 = T.x2a + b;
+    const int cc = (r == x1) + (r == x2) + (x1 == x2);
+    double v0 = K.base[cc];
+    if (SITE) v0 = __dadd_rn(v0, __dadd_rn(__dadd_rn(s0, T.s1[a]), T.s2[b]));
+    const double2 x1p = a == 1 ? nb.x1p[b] : mid.c[2 + b];
+    const double2 x1m = a == 0 ? nb.x1m[b] : mid.c[b];
+    const double2 x2p = b == 1 ? nb.x2p[a] : mid.c[2 * a + 1];
+    const double2 x2m = b == 0 ? nb.x2m[a] : mid.c[2 * a];
+    double2 h = rmul(v0, mid.c[q]);
+    h = madd<EXACT>(h, h0.y, dn.c[q]);        // particle 0 +move (plane r+1), hop[x0]
+    h = madd<EXACT>(h, h0.x, up.c[q]);        // particle 0 -move (plane r-1), hop[x0-1]
+    h = madd<EXACT>(h, T.h1[1 + a], x1p);     // particle 1 +move, hop[x1]
+    h = madd<EXACT>(h, T.h1[a], x1m);         // particle 1 -move, hop[x1-1]
+    h = madd<EXACT>(h, T.h2[1 + b], x2p);     // particle 2 +move, hop[x2]
+    h = madd<EXACT>(h, T.h2[b], x2m);         // particle 2 -move, hop[x2-1]
+    out.c[q] = times_i(ci, h);
+  }
+}
+
+__device__ __forceinline__ void store3(const T3& T, Piece3& P, int rr, const Quad& o, double& nrm) {
+  double2* base = P.dst + ((int64_t)rr * kN3 + T.x1a) * kN3 + T.x2a;
+  st256b(base, o.c[0], o.c[1]);
+  st256b(base + kN3, o.c[2], o.c[3]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) nrm += norm2(o.c[q]);
+  if ((rr + 1) % kPB == 0) {
+    double v = nrm;
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_down_sync(0xffffffffu, v, o2);
+    const int blk = rr / kPB;
+    if ((threadIdx.x & 31) == 0) red_tab()[(blk & 1) * 8 + (threadIdx.x >> 5)] = v;
+    nrm = 0.0;
+    P.pend = blk;
+  }
+}
+
+__device__ __forceinline__ void flush3(const T3& T, Piece3& P) {
+  if (P.pend >= 0 && threadIdx.x == 0) {
+    const double* red = red_tab() + (P.pend & 1) * 8;
+    double b = 0.0;
+    for (int w = 0; w < kThreads3 / 32; ++w) b += red[w];
+    P.part[P.pend * kCl + T.c] = b;
+  }
+  P.pend = -1;
+}
+
+// TMA: the ten x1 rows (x1a_band - 1 .. +8, wrapped) of psi plane y into slot.
+__device__ __forceinline__ void load_plane(const Plane3Args& a, const T3& T, const Piece3& P, int rho) {
+  if (threadIdx.x != 0) return;
+  const int y = wrap3(P.j0 - 1 + rho);
+  const int slot = rho % kRing3;
+  const uint32_t bar = bar_addr(slot);
+  const uint32_t dst0 = s_u32(smem3) + (uint32_t)slot * kPlaneB;
+  const int plane = (int)(P.g0 + y);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kPlaneB) : "memory");
+#pragma unroll
+  for (int t = 0; t < kTR; ++t) {
+    const int x1 = wrap3(T.c * kBand - 1 + t);
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];" ::"r"(dst0 + t * kRowB),
+        "l"(&a.tmap), "r"(0), "r"(0), "r"(x1), "r"(plane), "r"(bar)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void wait_plane(Piece3& P, int rho) {
+  if (rho <= P.last_rho) {
+    const int slot = rho % kRing3;
+    mbar_wait3(bar_addr(slot), (*P.ph >> slot) & 1u);
+    *P.ph ^= 1u << slot;
+  }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH, int K>
+__device__ __forceinline__ void plane3_stage(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i,
+                                             int j) {
+  constexpr double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
+  constexpr int s0 = ((PH - K + 1) % 3 + 3) % 3;
+  constexpr int sm = (s0 + 2) % 3;
+  constexpr int sp = (s0 + 1) % 3;
+  const int buf = i & 1;
+  const int rr = wrap3(j - K + 1);
+  const Nb nb = xch_nb(T, K - 2, buf ^ 1);
+  const double ci = RK4 ? a.ci[0] : a.ci[K - 1];
+  Quad tk;
+  apply3<EXACT, SITE>(T, a.k, rr, R.w[K - 1][sm], R.w[K - 1][s0], R.w[K - 1][sp], nb, ci, tk);
+  if constexpr (K == NAPP) {
+    const int jo = j - K + 1;
+    Quad o;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o.c[q] = RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]);
+    if (jo >= P.ya && jo < P.yb) store3(T, P, rr, o, R.nrm);
+  } else {
+    Quad nk;
+    if (RK4) {
+      const Quad pm = ring_quad<SC>(T, (i + (K == 2 ? 0 : kRing3 - 1)) % kRing3, P.s);  // psi(j-1) / psi(j-2)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nk.c[q] = K == 2 ? cadd(rmul(0.5, tk.c[q]), pm.c[q]) : cadd(tk.c[q], pm.c[q]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) R.acc[s0].c[q] = cadd(R.acc[s0].c[q], rmul(c13, tk.c[q]));
+    } else {
+      nk = tk;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) R.acc[s0].c[q] = cadd(R.acc[s0].c[q], tk.c[q]);
+    }
+    R.w[K][s0] = nk;
+    xch_put(T, K - 1, buf, nk);
+  }
+}
+
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH>
+__device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i) {
+  const int j = P.j0 + i;
+  wait_plane(P, i + 2);
+  cluster_sync_all();  // publishes last iteration's exchange planes cluster-wide, retires ring reads
+  flush3(T, P);
+  if (i + kPref3 + 1 <= P.last_rho) load_plane(a, T, P, i + kPref3 + 1);
+  const int buf = i & 1;
+  constexpr double c16 = 1.0 / 6.0;
+  constexpr int SM1 = (PH + 2) % 3;
+  const int r = wrap3(j);
+  const int sl_up = i % kRing3, sl_mid = (i + 1) % kRing3, sl_dn = (i + 2) % kRing3;
+  R.up = ring_quad<SC>(T, sl_up, P.s);
+  const Quad psi = ring_quad<SC>(T, sl_mid, P.s);
+  const Quad dn = ring_quad<SC>(T, sl_dn, P.s);
+  const Nb nb = ring_nb<SC>(T, sl_mid, P.s);
+  Quad t;
+  apply3<EXACT, SITE>(T, a.k, r, R.up, psi, dn, nb, a.ci[0], t);
+  Quad nt;
+  if (RK4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nt.c[q] = cadd(rmul(0.5, t.c[q]), psi.c[q]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t.c[q] = cadd(psi.c[q], rmul(c16, t.c[q]));
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) R.acc[SM1].c[q] = cadd(R.up.c[q], R.w[1][SM1].c[q]);
+    nt = t;
+  }
+  R.w[1][PH] = nt;
+  xch_put(T, 0, buf, nt);
+  if constexpr (NAPP >= 2) plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j);
+  if constexpr (NAPP >= 3) plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 3>(a, T, P, R, i, j);
+  if constexpr (NAPP >= 4) plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 4>(a, T, P, R, i, j);
+  if (RK4) R.acc[PH] = t;
+}
+
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC>
+__device__ __forceinline__ void plane3_loop(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R,
+                                            int iters) {
+#pragma unroll 1
+  for (int i = 0; i < iters; i += 3) {
+    plane3_iter<NAPP, RK4, SITE, EXACT, SC, 0>(a, T, P, R, i);
+    plane3_iter<NAPP, RK4, SITE, EXACT, SC, 1>(a, T, P, R, i + 1);
+    plane3_iter<NAPP, RK4, SITE, EXACT, SC, 2>(a, T, P, R, i + 2);
+  }
+}
+
+template <int NAPP, bool RK4, bool SITE, bool EXACT>
+__global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_constant__ Plane3Args a) {
+  static_assert(NAPP == 4, "plane3 pipelines four applications (Taylor-4 / RK4)");
+  cg::cluster_group cluster = cg::this_cluster();
+  const bool failed = *a.fail != kNoFail;  // uniform over the grid
+  if (failed) return;
+  if ((s_u32(smem3) & 1023u) != 0) __trap();  // TMA 128B swizzle needs 1024-byte aligned slots
+  T3 T;
+  T.c = (int)cluster.block_rank();
+  T.u = threadIdx.x >> 6;
+  T.v = threadIdx.x & 63;
+  T.x1a = T.c * kBand + 2 * T.u;
+  T.x2a = 2 * T.v;
+  T.up_nb = cluster.map_shared_rank(smem3, (T.c + kCl - 1) % kCl);
+  T.dn_nb = cluster.map_shared_rank(smem3, (T.c + 1) % kCl);
+  uint32_t ph_bits = 0;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kRing3; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_addr(q)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // the cluster's run of (realization, x0 block) work items
+  const int64_t nclus = gridDim.x / kCl;
+  const int64_t gid = blockIdx.x / kCl;
+  const int64_t total = a.count * kNblk3;
+  int64_t lo = total * gid / nclus;
+  const int64_t hi = total * (gid + 1) / nclus;
+  double2* hop2 = smem3 + kHopOff;
+  double* site = site_tab();
+  constexpr int64_t dim = (int64_t)kN3 * kN3 * kN3;
+  while (lo < hi) {
+    const int64_t r = lo / kNblk3;
+    const int b0 = (int)(lo % kNblk3);
+    const int nb = (int)std::min<int64_t>(hi - lo, kNblk3 - b0);
+    lo += nb;
+    Piece3 P;
+    P.ya = b0 * kPB;
+    P.yb = (b0 + nb) * kPB;
+    const double* hop = a.coef.hop + r * a.coef.stride;
+    const double* sg = SITE ? a.coef.site + r * a.coef.stride : nullptr;
+    cluster_sync_all();  // previous piece finished everywhere (tables, ring, exchange)
+    for (int y = threadIdx.x; y < kN3; y += kThreads3) {
+      hop2[y] = make_double2(hop[wrap3(y - 1)], hop[y]);
+      if (SITE) site[y] = sg[y];
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      T.h1[t] = hop[wrap3(T.x1a - 1 + t)];
+      T.h2[t] = hop[wrap3(T.x2a - 1 + t)];
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      T.s1[t] = SITE ? sg[T.x1a + t] : 0.0;
+      T.s2[t] = SITE ? sg[T.x2a + t] : 0.0;
+    }
+    P.s = a.scl ? a.scl[r] : 1.0;
+    P.scale = P.s != 1.0;
+    P.dst = a.psi_out + r * dim;
+    P.part = a.partial + r * (kNblk3 * kCl);
+    P.g0 = r * kN3;
+    P.pend = -1;
+    P.ph = &ph_bits;
+    P.j0 = P.ya - NAPP + 1;
+    const int iters = (P.yb - P.ya) + 2 * (NAPP - 1);
+    P.last_rho = iters + 1;
+    for (int rho = 0; rho <= kPref3; ++rho)
+      if (rho <= P.last_rho) load_plane(a, T, P, rho);
+    wait_plane(P, 0);
+    wait_plane(P, 1);
+    __syncthreads();
+    Regs3<NAPP> R;
+#pragma unroll
+    for (int k = 1; k < NAPP; ++k)
+#pragma unroll
+      for (int w = 0; w < 3; ++w)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) R.w[k][w].c[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < 3; ++w)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) R.acc[w].c[q] = make_double2(0.0, 0.0);
+    R.nrm = 0.0;
+    if (P.scale) plane3_loop<NAPP, RK4, SITE, EXACT, true>(a, T, P, R, iters);
+    else plane3_loop<NAPP, RK4, SITE, EXACT, false>(a, T, P, R, iters);
+    __syncthreads();
+    flush3(T, P);
+  }
+  cluster_sync_all();  // no CTA leaves while a neighbour may still read its exchange planes
+}
+
+int sm_count3() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+cudaError_t encode_planes_map(CUtensorMap* map, const double2* base, int64_t count) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!encode) return cudaErrorNotSupported;
+  if (count * kN3 > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const cuuint64_t dims[4] = {16, kN3 / 8, kN3, (cuuint64_t)(count * kN3)};
+  const cuuint64_t strides[3] = {128, (cuuint64_t)kRowB, (cuuint64_t)kRowB * kN3};
+  const cuuint32_t box[4] = {16, kN3 / 8, 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(base), dims, strides, box,
+                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int NAPP, bool RK4, bool SITE, bool EXACT>
+cudaError_t launch_p3(Plane3Args a, const double2* psi_in, cudaStream_t s) {
+  auto kern = plane3_kernel<NAPP, RK4, SITE, EXACT>;
+  static int nclus = 0;
+  if (nclus == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem3);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(kCl * 64, 1, 1);
+    cfg.blockDim = dim3(kThreads3, 1, 1);
+    cfg.dynamicSmemBytes = kSmem3;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    if (n < 1) return cudaErrorInvalidConfiguration;
+    nclus = n;
+  }
+  cudaError_t e = encode_planes_map(&a.tmap, psi_in, a.count);
+  if (e != cudaSuccess) return e;
+  const int64_t work = a.count * kNblk3;
+  const int64_t clusters = std::min<int64_t>(nclus, work);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(clusters * kCl), 1, 1);
+  cfg.blockDim = dim3(kThreads3, 1, 1);
+  cfg.dynamicSmemBytes = kSmem3;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+}  // namespace
+
+bool plane3_supported(int m, int n, const StepScalars& sc) {
+  return m == 3 && n == kN3 && (sc.backend == 1 || sc.order == 4);
+}
+
+int plane3_parts() { return kNblk3 * kCl; }
+
+cudaError_t launch_plane3_step(const double2* psi_in, double2* psi_out, int64_t count, const Coef& coef,
+                               const StencilConst& k, const StepScalars& sc, bool exact, const double* scl,
+                               double* partial, const long long* fail, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  Plane3Args a;
+  a.psi_out = psi_out;
+  a.count = count;
+  a.coef = coef;
+  a.k = k;
+  for (int i = 0; i < 4; ++i) a.ci[i] = sc.ci[i];
+  a.scl = scl;
+  a.partial = partial;
+  a.fail = fail;
+  const bool site = coef.site != nullptr;
+  const bool rk4 = sc.backend == 1;
+  if (rk4) {
+    if (site) return exact ? launch_p3<4, true, true, true>(a, psi_in, s) : launch_p3<4, true, true, false>(a, psi_in, s);
+    return exact ? launch_p3<4, true, false, true>(a, psi_in, s) : launch_p3<4, true, false, false>(a, psi_in, s);
+  }
+  if (site) return exact ? launch_p3<4, false, true, true>(a, psi_in, s) : launch_p3<4, false, true, false>(a, psi_in, s);
+  return exact ? launch_p3<4, false, false, true>(a, psi_in, s) : launch_p3<4, false, false, false>(a, psi_in, s);
+}
+
+}  // namespace ctqw

@@ -449,3 +449,30 @@ def test_band4_norm_partials_independent_of_batch(pkg, monkeypatch):
     h.bind(hop[137:138], site[137:138], 1, n)
     one, _ = run_evolve(h, psi0[137:138], 1, 30, stepper(dt=0.05))
     np.testing.assert_array_equal(full[137:138], one)
+
+
+PLANE3_CASES = [
+    # (B, backend, dt, steps, target)
+    (2, "taylor", 0.015, 3, "both"),     # pieces split realizations across clusters
+    (1, "rk4", 0.015, 2, "tunneling"),
+    (2, "taylor", 0.06, 3, "both"),      # renormalises every step (rescaled ring reads)
+]
+
+
+@pytest.mark.parametrize("case", PLANE3_CASES, ids=[f"B{c[0]}{c[1]}dt{c[2]}" for c in PLANE3_CASES])
+def test_plane3_m3_n128_matches_oracle(pkg, case):
+    """m = 3, N = 128 (configs[4]): the 16-CTA cluster kernel against the oracle."""
+    B, backend, dt, steps, target = case
+    n = 128
+    h, st, _keep = device_case(3, n, B, target)
+    psi0 = np.tile(orc.product_state(3, n), (B, 1))
+    mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, 4, dt))
+    assert h.step_kernel() == "plane3_kernel"
+    ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, 4)
+    assert_stats_match(stats, ostats)
+    if ostats.event_count == 0:
+        np.testing.assert_array_equal(mine, ref)
+    else:
+        assert np.abs(mine - ref).max() <= 1e-13
+    fma, _ = run_evolve(h, psi0, B, steps, stepper(backend, 4, dt, exact=False))
+    assert np.abs(fma - ref).max() <= 1e-12
