@@ -109,12 +109,18 @@ __device__ __forceinline__ uint32_t bar_addr(int slot) { return s_u32(red_tab() 
 struct T3 {
   int u, v, c;          // x1 pair, x2 pair, cluster rank (x1 band)
   int x1a, x2a;         // first owned x1 / x2
-  double h1[3];         // hop[x1a-1], hop[x1a], hop[x1a+1]
-  double h2[3];         // hop[x2a-1], hop[x2a], hop[x2a+1]
-  double s1[2], s2[2];  // site[x1a + a], site[x2a + b]
-  const double2* up_nb;   // x1 row above the band (DSMEM of rank c-1) for u == 0: exchange base
-  const double2* dn_nb;   // x1 row below the band (DSMEM of rank c+1) for u == 3
+  double h2[3];         // hop[x2a-1], hop[x2a], hop[x2a+1] (per lane: kept in registers)
+  double s2[2];         // site[x2a + b]
+  uint32_t up_nb;       // shared::cluster address of smem3 in rank c-1 (x1 row above the band)
+  uint32_t dn_nb;       // ... in rank c+1 (x1 row below the band)
 };
+
+__device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
+  double2 v;
+  // volatile: stays ordered after the cluster wait (asm volatile, memory clobber)
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
 
 struct Piece3 {
   double2* dst;
@@ -123,7 +129,7 @@ struct Piece3 {
   int j0, ya, yb, last_rho;
   double s;
   bool scale;
-  int pend;
+  int pend, pend2;
   uint32_t* ph;
 };
 
@@ -191,9 +197,9 @@ __device__ __forceinline__ Nb xch_nb(const T3& T, int k, int buf) {
     // rows across the band edge live in the neighbouring CTA (DSMEM);
     // u is warp-uniform, so these branches do not diverge
     if (T.u > 0) nb.x1m[t] = smem3[xoff(k, buf, 2 * T.u - 1, cm)];
-    else nb.x1m[t] = T.up_nb[xoff(k, buf, kBand - 1, cm)];
+    else nb.x1m[t] = ld_dsmem(T.up_nb + 16u * (uint32_t)xoff(k, buf, kBand - 1, cm));
     if (T.u < 3) nb.x1p[t] = smem3[xoff(k, buf, 2 * T.u + 2, cm)];
-    else nb.x1p[t] = T.dn_nb[xoff(k, buf, 0, cm)];
+    else nb.x1p[t] = ld_dsmem(T.dn_nb + 16u * (uint32_t)xoff(k, buf, 0, cm));
   }
   return nb;
 }
@@ -207,15 +213,26 @@ __device__ __forceinline__ void xch_put(const T3& T, int k, int buf, const Quad&
 template <bool EXACT, bool SITE>
 __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
                                        const Quad& dn, const Nb& nb, double ci, Quad& out) {
-  const double2 h0 = smem3[kHopOff + r];  // (hop[r-1], hop[r])
+  // couplings re-read from the shared table (hop2[y] = (hop[y-1], hop[y]))
+  // at every application: holding them in registers spills
+  const double2 h0 = smem3[kHopOff + r];
   const double s0 = SITE ? site_tab()[r] : 0.0;
+  const double2 h1a = smem3[kHopOff + T.x1a], h1b = smem3[kHopOff + T.x1a + 1];
+  const double h1[3] = {h1a.x, h1a.y, h1b.y};  // hop[x1a-1], hop[x1a], hop[x1a+1] (warp-uniform)
+  const double* h2 = T.h2;
+  const double* s2 = T.s2;
+  double s1[2] = {0.0, 0.0};
+  if (SITE) {
+    s1[0] = site_tab()[T.x1a];
+    s1[1] = site_tab()[T.x1a + 1];
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int a = q >> 1, b = q & 1;
     const int x1 = T.x1a + a, x2 = T.x2a + b;
     const int cc = (r == x1) + (r == x2) + (x1 == x2);
     double v0 = K.base[cc];
-    if (SITE) v0 = __dadd_rn(v0, __dadd_rn(__dadd_rn(s0, T.s1[a]), T.s2[b]));
+    if (SITE) v0 = __dadd_rn(v0, __dadd_rn(__dadd_rn(s0, s1[a]), s2[b]));
     const double2 x1p = a == 1 ? nb.x1p[b] : mid.c[2 + b];
     const double2 x1m = a == 0 ? nb.x1m[b] : mid.c[b];
     const double2 x2p = b == 1 ? nb.x2p[a] : mid.c[2 * a + 1];
@@ -223,10 +240,10 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
     double2 h = rmul(v0, mid.c[q]);
     h = madd<EXACT>(h, h0.y, dn.c[q]);        // particle 0 +move (plane r+1), hop[x0]
     h = madd<EXACT>(h, h0.x, up.c[q]);        // particle 0 -move (plane r-1), hop[x0-1]
-    h = madd<EXACT>(h, T.h1[1 + a], x1p);     // particle 1 +move, hop[x1]
-    h = madd<EXACT>(h, T.h1[a], x1m);         // particle 1 -move, hop[x1-1]
-    h = madd<EXACT>(h, T.h2[1 + b], x2p);     // particle 2 +move, hop[x2]
-    h = madd<EXACT>(h, T.h2[b], x2m);         // particle 2 -move, hop[x2-1]
+    h = madd<EXACT>(h, h1[1 + a], x1p);     // particle 1 +move, hop[x1]
+    h = madd<EXACT>(h, h1[a], x1m);         // particle 1 -move, hop[x1-1]
+    h = madd<EXACT>(h, h2[1 + b], x2p);     // particle 2 +move, hop[x2]
+    h = madd<EXACT>(h, h2[b], x2m);         // particle 2 -move, hop[x2-1]
     out.c[q] = times_i(ci, h);
   }
 }
@@ -248,14 +265,25 @@ __device__ __forceinline__ void store3(const T3& T, Piece3& P, int rr, const Qua
   }
 }
 
-__device__ __forceinline__ void flush3(const T3& T, Piece3& P) {
-  if (P.pend >= 0 && threadIdx.x == 0) {
-    const double* red = red_tab() + (P.pend & 1) * 8;
+// The warp partials of a finished norm block are written in the last stage,
+// after the iteration's cluster arrive, so thread 0 adds them up only after
+// the next arrive/wait pair: pend -> pend2 -> flushed.
+__device__ __forceinline__ void flush_blk3(const T3& T, Piece3& P, int blk) {
+  if (blk >= 0 && threadIdx.x == 0) {
+    const double* red = red_tab() + (blk & 1) * 8;
     double b = 0.0;
     for (int w = 0; w < kThreads3 / 32; ++w) b += red[w];
-    P.part[P.pend * kCl + T.c] = b;
+    P.part[blk * kCl + T.c] = b;
   }
+}
+__device__ __forceinline__ void flush3(const T3& T, Piece3& P, bool all = false) {
+  flush_blk3(T, P, P.pend2);
+  P.pend2 = P.pend;
   P.pend = -1;
+  if (all) {
+    flush_blk3(T, P, P.pend2);
+    P.pend2 = -1;
+  }
 }
 
 // TMA: the ten x1 rows (x1a_band - 1 .. +8, wrapped) of psi plane y into slot.
@@ -287,6 +315,12 @@ __device__ __forceinline__ void wait_plane(Piece3& P, int rho) {
   }
 }
 
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -294,14 +328,14 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH, int K>
 __device__ __forceinline__ void plane3_stage(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i,
-                                             int j) {
+                                             int j, const Nb* pre = nullptr) {
   constexpr double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
   constexpr int s0 = ((PH - K + 1) % 3 + 3) % 3;
   constexpr int sm = (s0 + 2) % 3;
   constexpr int sp = (s0 + 1) % 3;
   const int buf = i & 1;
   const int rr = wrap3(j - K + 1);
-  const Nb nb = xch_nb(T, K - 2, buf ^ 1);
+  const Nb nb = pre ? *pre : xch_nb(T, K - 2, buf ^ 1);
   const double ci = RK4 ? a.ci[0] : a.ci[K - 1];
   Quad tk;
   apply3<EXACT, SITE>(T, a.k, rr, R.w[K - 1][sm], R.w[K - 1][s0], R.w[K - 1][sp], nb, ci, tk);
@@ -334,7 +368,11 @@ template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH>
 __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i) {
   const int j = P.j0 + i;
   wait_plane(P, i + 2);
-  cluster_sync_all();  // publishes last iteration's exchange planes cluster-wide, retires ring reads
+  // the neighbours' exchange planes of the last iteration (own CTA's: the
+  // __syncthreads before the last signal)
+  // pairs with the arrive after stage 3 of the last iteration: its exchange
+  // planes are visible cluster-wide and its ring / exchange reads retired
+  if (i > 0) cluster_wait();
   flush3(T, P);
   if (i + kPref3 + 1 <= P.last_rho) load_plane(a, T, P, i + kPref3 + 1);
   const int buf = i & 1;
@@ -361,9 +399,16 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   }
   R.w[1][PH] = nt;
   xch_put(T, 0, buf, nt);
-  if constexpr (NAPP >= 2) plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j);
-  if constexpr (NAPP >= 3) plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 3>(a, T, P, R, i, j);
-  if constexpr (NAPP >= 4) plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 4>(a, T, P, R, i, j);
+  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j);
+  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 3>(a, T, P, R, i, j);
+  // The last stage publishes nothing: load its neighbours, then arrive, so
+  // the arrive's release waits only for stores of the previous iteration
+  // and the barrier latency overlaps the last stage.
+  // The last stage publishes nothing: load its neighbours, then arrive, so
+  // the barrier latency overlaps the last stage.
+  const Nb nb4 = xch_nb(T, NAPP - 2, buf ^ 1);
+  cluster_arrive();
+  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, NAPP>(a, T, P, R, i, j, &nb4);
   if (RK4) R.acc[PH] = t;
 }
 
@@ -391,8 +436,14 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
   T.v = threadIdx.x & 63;
   T.x1a = T.c * kBand + 2 * T.u;
   T.x2a = 2 * T.v;
-  T.up_nb = cluster.map_shared_rank(smem3, (T.c + kCl - 1) % kCl);
-  T.dn_nb = cluster.map_shared_rank(smem3, (T.c + 1) % kCl);
+  {
+    const uint32_t base = s_u32(smem3);
+    uint32_t up, dn;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(up) : "r"(base), "r"((T.c + kCl - 1) % kCl));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dn) : "r"(base), "r"((T.c + 1) % kCl));
+    T.up_nb = up;
+    T.dn_nb = dn;
+  }
   uint32_t ph_bits = 0;
   if (threadIdx.x == 0) {
     for (int q = 0; q < kRing3; ++q)
@@ -424,21 +475,16 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
       if (SITE) site[y] = sg[y];
     }
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      T.h1[t] = hop[wrap3(T.x1a - 1 + t)];
-      T.h2[t] = hop[wrap3(T.x2a - 1 + t)];
-    }
+    for (int t = 0; t < 3; ++t) T.h2[t] = hop[wrap3(T.x2a - 1 + t)];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      T.s1[t] = SITE ? sg[T.x1a + t] : 0.0;
-      T.s2[t] = SITE ? sg[T.x2a + t] : 0.0;
-    }
+    for (int t = 0; t < 2; ++t) T.s2[t] = SITE ? sg[T.x2a + t] : 0.0;
     P.s = a.scl ? a.scl[r] : 1.0;
     P.scale = P.s != 1.0;
     P.dst = a.psi_out + r * dim;
     P.part = a.partial + r * (kNblk3 * kCl);
     P.g0 = r * kN3;
     P.pend = -1;
+    P.pend2 = -1;
     P.ph = &ph_bits;
     P.j0 = P.ya - NAPP + 1;
     const int iters = (P.yb - P.ya) + 2 * (NAPP - 1);
@@ -462,8 +508,9 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     R.nrm = 0.0;
     if (P.scale) plane3_loop<NAPP, RK4, SITE, EXACT, true>(a, T, P, R, iters);
     else plane3_loop<NAPP, RK4, SITE, EXACT, false>(a, T, P, R, iters);
-    __syncthreads();
-    flush3(T, P);
+    cluster_wait();   // completes the last iteration's arrive
+    __syncthreads();  // the last stage has written its norm partials
+    flush3(T, P, true);
   }
   cluster_sync_all();  // no CTA leaves while a neighbour may still read its exchange planes
 }
