@@ -343,6 +343,7 @@ def ours(a):
     barrier()
     ms = start.elapsed_time(stop)
     kernel_ms, kernel_launches = h.kernel_time()
+    kernel = h.step_kernel()
     h.kernel_timing(False)
     launches = h.launches - launches0
     # the other arithmetic mode on the same states (reported beside the headline)
@@ -374,7 +375,6 @@ def ours(a):
     achieved = bytes_per_launch / (avg_launch_ms / 1000.0) / 1e9
     peak, peak_src = measured_peak_hbm()
     traffic = ncu_traffic()
-    kernel = h.step_kernel()
     traffic_bytes = None
     if traffic and traffic.get("kernel") == kernel and a.n == 256 and a.m == 2:
         # ncu --set full capture (profiles/), per realization-step, scaled to this launch

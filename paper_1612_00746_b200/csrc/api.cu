@@ -529,10 +529,7 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   // tests); a pinned family that does not support the case falls through
   // to the next one in auto order.
   const int kind = h->stream_kind;
-  // auto: RK4 in exact order runs faster on the warp-specialised one-column
-  // kernel for full-row N <= 512 (band4's RK4 carries one more row and spills)
-  const bool rk4_ws = kind == 0 && sc.backend == CTQW_BACKEND_RK4 && exact && h->n % 32 == 0 && h->n <= 512;
-  const bool use_band4 = (kind == 0 || kind == 4) && !rk4_ws && band4_supported(h->m, h->n, sc);
+  const bool use_band4 = (kind == 0 || kind == 4) && band4_supported(h->m, h->n, sc);
   const bool use_plane3 = (kind == 0 || kind == 5) && plane3_supported(h->m, h->n, sc);
   const bool use_band2 = !use_band4 && (kind == 0 || kind == 3 || kind == 4) &&
                          band2_supported(h->m, h->n, sc, exact, kind == 3);

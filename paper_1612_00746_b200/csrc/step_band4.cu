@@ -208,9 +208,23 @@ struct Lay4 {
   __device__ __forceinline__ static double* red(const Geo4<NN>& g) { return site(g) + (SITE ? g.n() : 0); }
   __device__ __forceinline__ static double* colc(const Geo4<NN>& g) { return red(g) + 64; }
   __device__ __forceinline__ static uint64_t* bars(const Geo4<NN>& g) {
-    return reinterpret_cast<uint64_t*>(colc(g) + 9 * g.np());
+    return reinterpret_cast<uint64_t*>(colc(g) + (SITE ? 9 : 5) * g.np());
+  }
+  // RK4: acc(j) = psi(j) + k1/6 parked from stage 1 to the end of the iteration
+  // ([q][NP], private per thread), instead of 16 registers across stages 2-4
+  __device__ __forceinline__ static double2* stash(const Geo4<NN>& g) {
+    const uintptr_t b = reinterpret_cast<uintptr_t>(bars(g) + kRing4);
+    return reinterpret_cast<double2*>((b + 15) & ~uintptr_t(15));
   }
 };
+
+// Does the RK4 stash fit next to the rest (compile-time sizes only)?
+constexpr bool stash_fits(int nn, bool site) {
+  return nn > 0 && (size_t)kRing4 * nn * 16 + (size_t)3 * 4 * (nn / 4) * 16 + (size_t)nn * 16 +
+                           (size_t)((site ? nn : 0) + 64 + (site ? 9 : 5) * (nn / 4)) * 8 + kRing4 * 8 + 16 +
+                           (size_t)4 * (nn / 4) * 16 <=
+                       227 * 1024;
+}
 
 // SC: multiply by the pending rescale s (the CTA's realization had a norm
 // correction last step); s == 1.0 otherwise, so skipping is exact.
@@ -425,9 +439,14 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
 #pragma unroll
       for (int q = 0; q < kCols; ++q) nt.c[q] = cadd(rmul(0.5, t.c[q]), psi.c[q]);
       // acc(j) = psi(j) + k1/6; slot PH still holds acc(j-3) until the last
-      // stage has consumed it, so the row waits in `t`.
+      // stage has consumed it, so the row waits in `t` (or in the stash).
 #pragma unroll
       for (int q = 0; q < kCols; ++q) t.c[q] = cadd(psi.c[q], rmul(c16, t.c[q]));
+      if constexpr (stash_fits(NN, SITE)) {
+        double2* st = L::stash(g);
+#pragma unroll
+        for (int q = 0; q < kCols; ++q) st[q * g.np() + T.p] = t.c[q];
+      }
     } else {
       // acc(j-1) = psi(j-1) + t1(j-1): both are at hand (psi(j-1) was just
       // read, t1(j-1) is window 1), and stage 2 below is its first update.
@@ -441,7 +460,15 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
     if constexpr (NAPP >= 2) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 2>(a, g, T, P, R, i, j);
     if constexpr (NAPP >= 3) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 3>(a, g, T, P, R, i, j);
     if constexpr (NAPP >= 4) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 4>(a, g, T, P, R, i, j);
-    if (RK4) R.acc[PH] = t;
+    if constexpr (RK4) {
+      if constexpr (stash_fits(NN, SITE)) {
+        const double2* st = L::stash(g);
+#pragma unroll
+        for (int q = 0; q < kCols; ++q) R.acc[PH].c[q] = st[q * g.np() + T.p];
+      } else {
+        R.acc[PH] = t;
+      }
+    }
   }
 }
 
@@ -593,8 +620,10 @@ Band4Plan plan_band4(int n, int napp, bool site, int64_t count) {
   p.nblk = n / p.rb;
   const int nx = napp > 1 ? napp - 1 : 1;
   p.smem = (size_t)kRing4 * p.npad * sizeof(double2) + (size_t)nx * 4 * p.threads * sizeof(double2) +
-           (size_t)n * sizeof(double2) + (size_t)((site ? n : 0) + 64 + 9 * p.threads) * sizeof(double) +
+           (size_t)n * sizeof(double2) + (size_t)((site ? n : 0) + 64 + (site ? 9 : 5) * p.threads) * sizeof(double) +
            kRing4 * sizeof(uint64_t);
+  if (napp == 4 && (n == 256 || n == 512 || n == 1024) && stash_fits(n, site))
+    p.smem += 16 + (size_t)4 * p.threads * sizeof(double2);  // RK4 stash (also sized for Taylor-4: harmless)
   return p;
 }
 
