@@ -17,6 +17,11 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+try:
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as _f:
+        PEAK = float(json.load(_f)["hbm_gbs"]) * 1e9
+except Exception:
+    PEAK = 6544e9
 
 
 def timed(ens, cfg, steps, post_rate, engine, torch):
@@ -39,7 +44,7 @@ def timed(ens, cfg, steps, post_rate, engine, torch):
 
 
 def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling", post_rates=(None,),
-             exact=True, observables=("populations", "position_mean_variance", "participation_ratio")):
+             observables=("populations", "position_mean_variance", "participation_ratio")):
     import torch
 
     import paper_1612_00746_b200 as p
@@ -49,21 +54,25 @@ def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling"
                       noise=p.NoiseSpec(target=target, levels=(-0.1, 0.1), rate=0.0),
                       stepper=p.StepperConfig(backend=backend, dt=dt), realizations=R, steps=steps,
                       post_rate=steps, precision="double", observables=observables,
-                      memory_budget=175 * 2**30, exact=exact, device=0)
+                      memory_budget=175 * 2**30, exact=False, device=0)
     ens = engine.EnsembleState(cfg, 0, 0, R)
     ens.evolve(0, 2)
     ens.stats()
     engine.collect_observables(cfg, ens)
     out = []
-    for pr in post_rates:
-        prate = steps if pr is None else pr
-        secs = timed(ens, cfg, steps, prate, engine, torch)
-        rate = R * steps / secs
-        line = {"case": name, "m": m, "n": n, "realizations": R, "steps": steps, "backend": backend,
-                "post_rate": prate, "exact": exact, "seconds": secs, "r_steps_per_s": rate,
-                "hbm_frac_of_measured": rate * 32.0 * n ** m / 6459e9}
-        print(json.dumps(line), flush=True)
-        out.append(line)
+    for ex in (False, True):  # FMA-contracted, then exact reference order
+        ens.stepper = cfg.stepper.native(ex)
+        ens.evolve(0, 1)
+        for pr in post_rates:
+            prate = steps if pr is None else pr
+            secs = timed(ens, cfg, steps, prate, engine, torch)
+            rate = R * steps / secs
+            line = {"case": name, "m": m, "n": n, "realizations": R, "steps": steps, "backend": backend,
+                    "post_rate": prate, "exact": ex, "seconds": secs, "r_steps_per_s": rate,
+                    "kernel": ens.handle.step_kernel(),
+                    "hbm_frac_of_measured": rate * 32.0 * n ** m / PEAK}
+            print(json.dumps(line), flush=True)
+            out.append(line)
     del ens
     torch.cuda.empty_cache()
     return out
@@ -86,8 +95,9 @@ def main():
     # configs[3]: N=512, post-processing frequency sweep
     run_case("configs[3] N=512 R=1000 post sweep", 2, 512, 1000, 100 if q else 1000,
              post_rates=(1, 10, 100, None) if not q else (1, 10, None))
-    # configs[4]: m=3, N=128 (D=2^21), generic path
-    run_case("configs[4] m=3 N=128 R=512", 3, 128, 512, 5 if q else 20, dt=0.015)
+    # configs[4]: m=3, N=128 (D=2^21), 16-CTA cluster kernel; the largest ensemble that fits
+    # (two 32 MiB buffers per realization) is ~2600 per GPU -- R=2048 here
+    run_case("configs[4] m=3 N=128 R=2048", 3, 128, 2048, 5 if q else 20, dt=0.015)
 
 
 if __name__ == "__main__":
