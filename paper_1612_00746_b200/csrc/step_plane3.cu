@@ -133,10 +133,15 @@ struct Piece3 {
   uint32_t* ph;
 };
 
+// Carried state.  Every stage output plane is published in full to the
+// CTA's exchange buffer (the neighbours need all of it), so a window keeps
+// only its oldest row in registers: the middle row is re-read from the
+// exchange buffer (last iteration's parity) and the newest comes from the
+// stage that just produced it.
 template <int NAPP>
 struct Regs3 {
-  Quad w[NAPP][3];
-  Quad acc[3];
+  Quad old[NAPP];  // old[k]: stage-k output, row (plane) j-k-1 at iteration j; old[0] unused
+  Quad acc[3];     // running sums, slot = row mod 3 (relative)
   Quad up;
   double nrm;
 };
@@ -202,6 +207,13 @@ __device__ __forceinline__ Nb xch_nb(const T3& T, int k, int buf) {
     else nb.x1p[t] = ld_dsmem(T.dn_nb + 16u * (uint32_t)xoff(k, buf, 0, cm));
   }
   return nb;
+}
+
+__device__ __forceinline__ Quad xch_own(const T3& T, int k, int buf) {
+  Quad v;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v.c[q] = smem3[xoff(k, buf, 2 * T.u + (q >> 1), 2 * T.v + (q & 1))];
+  return v;
 }
 
 __device__ __forceinline__ void xch_put(const T3& T, int k, int buf, const Quad& v) {
@@ -307,11 +319,20 @@ __device__ __forceinline__ void load_plane(const Plane3Args& a, const T3& T, con
   }
 }
 
+// Wait for ring plane rho; if the realization carries a pending norm
+// correction, scale the landed tile once in shared memory (rmul(s, psi) is
+// exactly what the reference's in-place rescale stores), so the compute loop
+// has a single variant.  The caller's next __syncthreads publishes the writes.
 __device__ __forceinline__ void wait_plane(Piece3& P, int rho) {
   if (rho <= P.last_rho) {
     const int slot = rho % kRing3;
     mbar_wait3(bar_addr(slot), (*P.ph >> slot) & 1u);
     *P.ph ^= 1u << slot;
+    if (P.scale) {
+      double2* tile = smem3 + slot * kTR * kN3;
+      for (int e = threadIdx.x; e < kTR * kN3; e += kThreads3) tile[e] = rmul(P.s, tile[e]);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // before TMA rewrites the slot
+    }
   }
 }
 
@@ -326,28 +347,28 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// Stage K (2..NAPP) of iteration j: plane j-K+1 from (old, mid, dn) =
+// stage K-1's planes j-K, j-K+1, j-K+2 and the in-plane neighbours of the
+// middle one.  Returns the stage's output (the next stage's dn).
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH, int K>
-__device__ __forceinline__ void plane3_stage(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i,
-                                             int j, const Nb* pre = nullptr) {
+__device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i,
+                                             int j, const Quad& mid, const Quad& dn, const Nb& nb) {
   constexpr double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
-  constexpr int s0 = ((PH - K + 1) % 3 + 3) % 3;
-  constexpr int sm = (s0 + 2) % 3;
-  constexpr int sp = (s0 + 1) % 3;
+  constexpr int s0 = ((PH - K + 1) % 3 + 3) % 3;  // acc slot of plane j-K+1
   const int buf = i & 1;
   const int rr = wrap3(j - K + 1);
-  const Nb nb = pre ? *pre : xch_nb(T, K - 2, buf ^ 1);
   const double ci = RK4 ? a.ci[0] : a.ci[K - 1];
   Quad tk;
-  apply3<EXACT, SITE>(T, a.k, rr, R.w[K - 1][sm], R.w[K - 1][s0], R.w[K - 1][sp], nb, ci, tk);
+  apply3<EXACT, SITE>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk);
+  R.old[K - 1] = mid;
+  Quad nk;
   if constexpr (K == NAPP) {
     const int jo = j - K + 1;
-    Quad o;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      o.c[q] = RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]);
-    if (jo >= P.ya && jo < P.yb) store3(T, P, rr, o, R.nrm);
+      nk.c[q] = RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]);
+    if (jo >= P.ya && jo < P.yb) store3(T, P, rr, nk, R.nrm);
   } else {
-    Quad nk;
     if (RK4) {
       const Quad pm = ring_quad<SC>(T, (i + (K == 2 ? 0 : kRing3 - 1)) % kRing3, P.s);  // psi(j-1) / psi(j-2)
 #pragma unroll
@@ -359,9 +380,9 @@ __device__ __forceinline__ void plane3_stage(const Plane3Args& a, const T3& T, P
 #pragma unroll
       for (int q = 0; q < 4; ++q) R.acc[s0].c[q] = cadd(R.acc[s0].c[q], tk.c[q]);
     }
-    R.w[K][s0] = nk;
     xch_put(T, K - 1, buf, nk);
   }
+  return nk;
 }
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH>
@@ -373,6 +394,10 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   // pairs with the arrive after stage 3 of the last iteration: its exchange
   // planes are visible cluster-wide and its ring / exchange reads retired
   if (i > 0) cluster_wait();
+  // The wait pairs with arrives made before this thread's (and every other
+  // thread's) wait_plane above, so it does not order the rescale writes of
+  // wait_plane; a CTA barrier does.  Only pieces with a pending rescale pay it.
+  if (i == 0 || P.scale) __syncthreads();
   flush3(T, P);
   if (i + kPref3 + 1 <= P.last_rho) load_plane(a, T, P, i + kPref3 + 1);
   const int buf = i & 1;
@@ -386,6 +411,7 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   const Nb nb = ring_nb<SC>(T, sl_mid, P.s);
   Quad t;
   apply3<EXACT, SITE>(T, a.k, r, R.up, psi, dn, nb, a.ci[0], t);
+  const Quad mid1 = xch_own(T, 0, buf ^ 1);  // t1 (arg1) of plane j-1
   Quad nt;
   if (RK4) {
 #pragma unroll
@@ -393,22 +419,21 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
 #pragma unroll
     for (int q = 0; q < 4; ++q) t.c[q] = cadd(psi.c[q], rmul(c16, t.c[q]));
   } else {
+    // acc(j-1) = psi(j-1) + t1(j-1); stage 2 below is its first update
 #pragma unroll
-    for (int q = 0; q < 4; ++q) R.acc[SM1].c[q] = cadd(R.up.c[q], R.w[1][SM1].c[q]);
+    for (int q = 0; q < 4; ++q) R.acc[SM1].c[q] = cadd(R.up.c[q], mid1.c[q]);
     nt = t;
   }
-  R.w[1][PH] = nt;
   xch_put(T, 0, buf, nt);
-  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j);
-  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 3>(a, T, P, R, i, j);
-  // The last stage publishes nothing: load its neighbours, then arrive, so
-  // the arrive's release waits only for stores of the previous iteration
-  // and the barrier latency overlaps the last stage.
-  // The last stage publishes nothing: load its neighbours, then arrive, so
-  // the barrier latency overlaps the last stage.
+  const Quad t2 = plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
+  const Quad t3 = plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 3>(a, T, P, R, i, j, xch_own(T, 1, buf ^ 1), t2,
+                                                                  xch_nb(T, 1, buf ^ 1));
+  // The last stage publishes nothing: load what it reads from the exchange
+  // buffers, then arrive, so the barrier latency overlaps the last stage.
   const Nb nb4 = xch_nb(T, NAPP - 2, buf ^ 1);
+  const Quad mid4 = xch_own(T, NAPP - 2, buf ^ 1);
   cluster_arrive();
-  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, NAPP>(a, T, P, R, i, j, &nb4);
+  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, NAPP>(a, T, P, R, i, j, mid4, t3, nb4);
   if (RK4) R.acc[PH] = t;
 }
 
@@ -496,18 +521,15 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     __syncthreads();
     Regs3<NAPP> R;
 #pragma unroll
-    for (int k = 1; k < NAPP; ++k)
+    for (int k = 0; k < NAPP; ++k)
 #pragma unroll
-      for (int w = 0; w < 3; ++w)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) R.w[k][w].c[q] = make_double2(0.0, 0.0);
+      for (int q = 0; q < 4; ++q) R.old[k].c[q] = make_double2(0.0, 0.0);
 #pragma unroll
     for (int w = 0; w < 3; ++w)
 #pragma unroll
       for (int q = 0; q < 4; ++q) R.acc[w].c[q] = make_double2(0.0, 0.0);
     R.nrm = 0.0;
-    if (P.scale) plane3_loop<NAPP, RK4, SITE, EXACT, true>(a, T, P, R, iters);
-    else plane3_loop<NAPP, RK4, SITE, EXACT, false>(a, T, P, R, iters);
+    plane3_loop<NAPP, RK4, SITE, EXACT, false>(a, T, P, R, iters);  // ring tiles arrive pre-scaled
     cluster_wait();   // completes the last iteration's arrive
     __syncthreads();  // the last stage has written its norm partials
     flush3(T, P, true);
@@ -616,12 +638,16 @@ cudaError_t launch_plane3_step(const double2* psi_in, double2* psi_out, int64_t 
   a.fail = fail;
   const bool site = coef.site != nullptr;
   const bool rk4 = sc.backend == 1;
+#ifdef P3_ONLY  // register-pressure experiments: one instantiation
+  return launch_p3<4, false, false, false>(a, psi_in, s);
+#else
   if (rk4) {
     if (site) return exact ? launch_p3<4, true, true, true>(a, psi_in, s) : launch_p3<4, true, true, false>(a, psi_in, s);
     return exact ? launch_p3<4, true, false, true>(a, psi_in, s) : launch_p3<4, true, false, false>(a, psi_in, s);
   }
   if (site) return exact ? launch_p3<4, false, true, true>(a, psi_in, s) : launch_p3<4, false, true, false>(a, psi_in, s);
   return exact ? launch_p3<4, false, false, true>(a, psi_in, s) : launch_p3<4, false, false, false>(a, psi_in, s);
+#endif
 }
 
 }  // namespace ctqw

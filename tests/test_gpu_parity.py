@@ -476,3 +476,19 @@ def test_plane3_m3_n128_matches_oracle(pkg, case):
         assert np.abs(mine - ref).max() <= 1e-13
     fma, _ = run_evolve(h, psi0, B, steps, stepper(backend, 4, dt, exact=False))
     assert np.abs(fma - ref).max() <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,B,family", [(3, 128, 2, "plane3"), (2, 256, 300, "band4"), (2, 1024, 6, "band4")])
+def test_streaming_kernels_bitwise_repeatable(pkg, monkeypatch, m, n, B, family):
+    """Repeat runs with a renormalisation every step are bit-identical (catches
+    ordering races in the ring / exchange / norm-partial paths)."""
+    monkeypatch.setenv("CTQW_STREAM", family)
+    h, _, _keep = device_case(m, n, B, "both")
+    psi0 = np.tile(orc.product_state(m, n), (B, 1))
+    dt = 0.06 if m == 3 else 0.08
+    for exact in (True, False):
+        first, s0 = run_evolve(h, psi0, B, 3, stepper("taylor", 4, dt, exact=exact))
+        assert s0.corrections > 0
+        for _ in range(3):
+            again, _ = run_evolve(h, psi0, B, 3, stepper("taylor", 4, dt, exact=exact))
+            np.testing.assert_array_equal(first, again)
