@@ -187,9 +187,12 @@ __device__ __forceinline__ Nb ring_nb(const T3& T, int slot, double s) {
   return nb;
 }
 
-// exchange element of stage k (0-based output index), parity buf
+// exchange element of stage k (0-based output index), parity buf.  Rows are
+// stored even columns first, then odd ones: every access pattern on them
+// (columns 2v+b, 2v-1, 2v+2 across a warp) is then bank-conflict free,
+// which the TMA swizzle is not for the +-1 shifted ones.
 __device__ __forceinline__ int xoff(int k, int buf, int row, int col) {
-  return kXOff + k * kXStage + (buf * kBand + row) * kN3 + swz3(col);
+  return kXOff + k * kXStage + (buf * kBand + row) * kN3 + (col & 1) * (kN3 / 2) + (col >> 1);
 }
 
 __device__ __forceinline__ Nb xch_nb(const T3& T, int k, int buf) {
