@@ -116,6 +116,29 @@ int ctqw_draw_noise(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64_t c
  * (hamiltonian.py:134-135).  n_links is 0 or N, n_sites is 0 or N.
  * hop_dev is [count][N]; site_dev is [count][N] and is written only when
  * n_sites == N. */
+/* Dynamic (random-telegraph) noise, rate > 0: the reference's NoiseProcess
+ * (noise.py:71-206).  ctqw_telegraph_init draws, per realization
+ * r0 .. r0+count-1, values = choice(levels, total) and next_switch =
+ * exponential(1/rate, total) from default_rng((master_seed, r)) -- bit-exact
+ * to NumPy -- into library-owned buffers ([count][n_links + n_sites], links
+ * first); ctqw_telegraph_values returns them (device pointer) for
+ * ctqw_build_coefficients.  Once enabled, ctqw_evolve advances the process
+ * by dt after every step's norm check and rewrites the bound hop/site rows of
+ * switched elements (ensemble.py:536-544, hamiltonian.py:164-192).
+ * ctqw_telegraph_read copies values / switch times (device to device) and
+ * per-realization time and switch counts (to the host); any pointer may be
+ * NULL. */
+int ctqw_telegraph_init(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64_t count,
+                        const double *levels_host, int32_t n_levels, int64_t n_links, int64_t n_sites,
+                        double rate, void *stream);
+const double *ctqw_telegraph_values(ctqw_handle_t h);
+/* advance(process, dt) for realizations 0 .. count-1 without a step
+ * (noise.py:175-206); rewrites bound coefficients of switched elements. */
+int ctqw_telegraph_advance(ctqw_handle_t h, int64_t count, double dt, void *stream);
+int ctqw_telegraph_enable(ctqw_handle_t h, int32_t enable);
+int ctqw_telegraph_read(ctqw_handle_t h, double *values_dev, double *next_switch_dev, double *times_host,
+                        int64_t *switches_host, void *stream);
+
 int ctqw_build_coefficients(ctqw_handle_t h, const double *noise_dev, int64_t count,
                             int64_t n_links, int64_t n_sites, double *hop_dev,
                             double *site_dev, void *stream);

@@ -224,9 +224,22 @@ class SegmentStats:
     max_deviation: float = 0.0
 
 
+def refresh_stencil(st, noise, tunneling):
+    """Couplings after a telegraph advance: a fresh ``assemble_values``
+    (hamiltonian.py:131-141), which the reference's incremental ``update``
+    reproduces bit for bit (test_hamiltonian.py:124-139)."""
+    if noise.n_links:
+        st.hop = np.float64(tunneling) + noise.link_values()
+    if noise.n_sites:
+        st.site = noise.site_values().copy()
+
+
 def evolve_segment(st, psi, start_step, n_steps, dt, hbar=1.0, backend="taylor", order=4,
-                   tol_norm=1e-6, tol_fail=1e-3, renormalize=True, r0=0):
-    """Advance a (B, D) stack ``n_steps`` with the per-step norm policy."""
+                   tol_norm=1e-6, tol_fail=1e-3, renormalize=True, r0=0, noise=None, tunneling=1.0):
+    """Advance a (B, D) stack ``n_steps`` with the per-step norm policy.
+
+    ``noise`` (a ``TelegraphOracle``) is advanced by ``dt`` after every
+    step's norm check and the couplings rebuilt (ensemble.py:536-544)."""
     v0 = diagonal_values(st)
     stats = SegmentStats()
     for s in range(n_steps):
@@ -247,6 +260,10 @@ def evolve_segment(st, psi, start_step, n_steps, dt, hbar=1.0, backend="taylor",
                 stats.event_count += 1
                 if len(stats.events) < MAX_EVENTS_PER_SEGMENT:
                     stats.events.append((float(dev[row]), bool(corrected[row]), r0 + int(row), step_number))
+        if noise is not None:
+            noise.advance(dt)
+            refresh_stencil(st, noise, tunneling)
+            v0 = diagonal_values(st)
     return psi, stats
 
 
@@ -333,7 +350,7 @@ def schedule(steps: int, post_rate: int):
 
 def run_rows(st, psi0, realizations, steps, post_rate, dt, hbar=1.0, backend="taylor", order=4,
              observables=("populations", "position_mean_variance", "purity", "participation_ratio"),
-             tol_norm=1e-6, tol_fail=1e-3, renormalize=True):
+             tol_norm=1e-6, tol_fail=1e-3, renormalize=True, noise=None, tunneling=1.0):
     """Diagonal-observable restatement of ``run`` (ensemble.py:635-804)."""
     psi = np.tile(psi0, (realizations, 1))
     out = []
@@ -343,7 +360,7 @@ def run_rows(st, psi0, realizations, steps, post_rate, dt, hbar=1.0, backend="ta
         span = target - prev
         if span > 0:
             psi, stats = evolve_segment(st, psi, prev, span, dt, hbar, backend, order,
-                                        tol_norm, tol_fail, renormalize)
+                                        tol_norm, tol_fail, renormalize, noise=noise, tunneling=tunneling)
             totals.event_count += stats.event_count
             totals.corrections += stats.corrections
             totals.max_deviation = max(totals.max_deviation, stats.max_deviation)

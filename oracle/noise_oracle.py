@@ -171,3 +171,51 @@ def draw_static_noise_stack(master_seed: int, r0: int, count: int, levels, total
     for i in range(count):
         out[i] = draw_static_noise(master_seed, r0 + i, levels, total)
     return out
+
+
+class TelegraphOracle:
+    """Dynamic telegraph noise of a batch of realizations (TEST ONLY).
+
+    Restates ``init_process`` / ``advance`` (``pkg/src/ctqw/noise.py:128-206``)
+    for ``rate > 0``.  The arithmetic of those functions is NumPy's
+    ``Generator`` (``choice`` and ``exponential``, the ziggurat sampler of
+    numpy/random/src/distributions/distributions.c); it is called here as
+    the reference calls it, with one ``default_rng((master_seed, r))`` per
+    realization (``ensemble.py:680-682``), so this is the reference algorithm
+    on the same streams.  ``values``/``next_switch`` are laid out
+    ``[links | sites]`` per realization.
+    """
+
+    def __init__(self, master_seed, r0, count, levels, n_links, n_sites, rate):
+        self.levels = np.asarray(levels, dtype=np.float64)
+        self.n_links, self.n_sites = int(n_links), int(n_sites)
+        total = self.n_links + self.n_sites
+        self.mean_wait = 1.0 / float(rate)
+        self.rngs = [np.random.default_rng((int(master_seed), int(r))) for r in range(r0, r0 + count)]
+        self.values = np.empty((count, total))
+        self.next_switch = np.empty((count, total))
+        for i, g in enumerate(self.rngs):          # noise.py:152-157
+            self.values[i] = g.choice(self.levels, size=total)
+            self.next_switch[i] = g.exponential(1.0 / float(rate), size=total)
+        self.time = np.zeros(count)
+        self.switches = np.zeros(count, dtype=np.int64)
+
+    def advance(self, dt):
+        """``advance(process, dt)`` for every realization (noise.py:175-206)."""
+        for i, g in enumerate(self.rngs):
+            t_end = self.time[i] + dt
+            due = self.next_switch[i] <= t_end
+            if self.values.shape[1] and due.any():
+                idx = np.nonzero(due)[0]
+                while idx.size:
+                    self.switches[i] += idx.size
+                    self.values[i, idx] = g.choice(self.levels, size=idx.size)
+                    self.next_switch[i, idx] += g.exponential(self.mean_wait, size=idx.size)
+                    idx = idx[self.next_switch[i, idx] <= t_end]
+            self.time[i] = t_end
+
+    def link_values(self):
+        return self.values[:, : self.n_links]
+
+    def site_values(self):
+        return self.values[:, self.n_links:]

@@ -56,6 +56,16 @@ struct ctqw_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int64_t timed_launches = 0;
+  // dynamic telegraph noise (rate > 0): library-owned process state
+  double* tg_values = nullptr;      // [count][total]
+  double* tg_next = nullptr;        // [count][total] next switch times
+  TelegraphGen* tg_gen = nullptr;   // [count] generator, time, switch count
+  double* tg_levels = nullptr;
+  int64_t tg_cap = 0, tg_gen_cap = 0, tg_count = 0, tg_total = 0, tg_links = 0, tg_sites = 0;
+  int tg_nlev = 0;
+  double tg_mean_wait = 0.0;
+  bool tg_enabled = false;
+  long long* tg_sum = nullptr;
   int stream_kind = 0;  // CTQW_STREAM: 0 auto, 1 tile, 2 band, 3 band2, 4 band4, 5 plane3, 6 generic
   const char* stream_kernel = "";  // dominant kernel of the last ctqw_evolve
   std::string err;
@@ -251,6 +261,19 @@ int generic_step(ctqw_ctx* h, const ctqw_stepper_t* st, const StepScalars& sc, c
   return CTQW_OK;
 }
 
+// Advance the bound telegraph process by dt and rewrite the couplings of
+// switched elements (ensemble.py:536-544); a no-op for static noise.
+int telegraph_step(ctqw_ctx* h, int64_t count, double dt, cudaStream_t s) {
+  if (!h->tg_enabled) return CTQW_OK;
+  if (count > h->tg_count) return fail_with(h, CTQW_ERR_CONFIG, "more realizations than the noise process holds");
+  CUDA_TRY(h, launch_telegraph_advance(count, h->tg_total, h->tg_links, h->tg_sites, h->n, dt, h->tg_levels,
+                                       h->tg_nlev, h->tg_mean_wait, h->model.tunneling, h->tg_values, h->tg_next,
+                                       h->tg_gen, const_cast<double*>(h->hop), const_cast<double*>(h->site),
+                                       h->stride, h->fail, s));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -324,7 +347,7 @@ int ctqw_destroy(ctqw_handle_t h) {
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   void* dev_ptrs[] = {h->levels, h->partial, h->scl, h->stats, h->events, h->fail,
                       h->summary_dev, h->scratch[0], h->scratch[1], h->n2_dev, h->small,
-                      h->overlap_partial};
+                      h->overlap_partial, h->tg_values, h->tg_next, h->tg_gen, h->tg_levels, h->tg_sum};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (h->summary_host) cudaFreeHost(h->summary_host);
@@ -350,6 +373,97 @@ int ctqw_draw_noise(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64_t c
   // levels_host may be freed by the caller after return
   CUDA_TRY(h, cudaStreamSynchronize(s));
   h->launches += 1;
+  return CTQW_OK;
+}
+
+int ctqw_telegraph_init(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64_t count,
+                        const double* levels_host, int32_t n_levels, int64_t n_links, int64_t n_sites,
+                        double rate, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (n_levels < 1 || !levels_host) return fail_with(h, CTQW_ERR_CONFIG, "noise level set is empty");
+  if (r0 < 0 || count < 0 || n_links < 0 || n_sites < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative sizes");
+  if ((n_links != 0 && n_links != h->n) || (n_sites != 0 && n_sites != h->n))
+    return fail_with(h, CTQW_ERR_CONFIG, "noise rows must hold 0 or N links and 0 or N sites");
+  if (!(rate > 0.0) || !std::isfinite(rate)) return fail_with(h, CTQW_ERR_CONFIG, "telegraph rate must be > 0");
+  for (int i = 0; i < n_levels; ++i)
+    if (!std::isfinite(levels_host[i])) return fail_with(h, CTQW_ERR_CONFIG, "noise levels must be finite");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t total = n_links + n_sites;
+  int rc = ensure(h, &h->tg_values, &h->tg_cap, count * total, "telegraph values");
+  if (rc) return rc;
+  if (h->tg_next) cudaFree(h->tg_next);
+  h->tg_next = nullptr;
+  if (count * total > 0 && cudaMalloc(&h->tg_next, count * total * sizeof(double)) != cudaSuccess)
+    return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate telegraph switch times");
+  if (h->tg_gen) cudaFree(h->tg_gen);
+  h->tg_gen = nullptr;
+  if (count > 0 && cudaMalloc(&h->tg_gen, count * sizeof(TelegraphGen)) != cudaSuccess)
+    return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate telegraph generators");
+  if (h->tg_levels) cudaFree(h->tg_levels);
+  h->tg_levels = nullptr;
+  if (cudaMalloc(&h->tg_levels, n_levels * sizeof(double)) != cudaSuccess)
+    return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate noise levels");
+  CUDA_TRY(h, cudaMemcpyAsync(h->tg_levels, levels_host, n_levels * sizeof(double), cudaMemcpyHostToDevice, s));
+  h->tg_count = count;
+  h->tg_total = total;
+  h->tg_links = n_links;
+  h->tg_sites = n_sites;
+  h->tg_nlev = n_levels;
+  h->tg_mean_wait = 1.0 / rate;  // noise.py:112 (_mean_wait = 1.0 / spec.rate)
+  h->tg_enabled = false;
+  if (total > 0)
+    CUDA_TRY(h, launch_telegraph_init(master_seed, r0, count, h->tg_levels, n_levels, total, h->tg_mean_wait,
+                                      h->tg_values, h->tg_next, h->tg_gen, s));
+  CUDA_TRY(h, cudaStreamSynchronize(s));  // levels_host may be freed by the caller after return
+  h->launches += 1;
+  return CTQW_OK;
+}
+
+const double* ctqw_telegraph_values(ctqw_handle_t h) { return h ? h->tg_values : nullptr; }
+
+int ctqw_telegraph_advance(ctqw_handle_t h, int64_t count, double dt, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (!(dt >= 0.0) || !std::isfinite(dt)) return fail_with(h, CTQW_ERR_CONFIG, "advance window dt must be >= 0");
+  if (count < 0 || count > h->tg_count) return fail_with(h, CTQW_ERR_CONFIG, "count exceeds the noise process");
+  if (h->tg_total == 0 || count == 0) return CTQW_OK;
+  DeviceGuard g(h->device);
+  const bool coef = h->hop && h->coef_count >= count;
+  CUDA_TRY(h, launch_telegraph_advance(count, h->tg_total, h->tg_links, h->tg_sites, h->n, dt, h->tg_levels,
+                                       h->tg_nlev, h->tg_mean_wait, h->model.tunneling, h->tg_values, h->tg_next,
+                                       h->tg_gen, coef ? const_cast<double*>(h->hop) : nullptr,
+                                       coef ? const_cast<double*>(h->site) : nullptr, h->stride, nullptr,
+                                       (cudaStream_t)stream));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
+int ctqw_telegraph_enable(ctqw_handle_t h, int32_t enable) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (enable && h->tg_total > 0 && !h->tg_values)
+    return fail_with(h, CTQW_ERR_CONFIG, "no telegraph process (ctqw_telegraph_init)");
+  h->tg_enabled = enable != 0 && h->tg_total > 0;
+  return CTQW_OK;
+}
+
+int ctqw_telegraph_read(ctqw_handle_t h, double* values_dev, double* next_switch_dev, double* times_host,
+                        int64_t* switches_host, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)h->tg_count * h->tg_total * sizeof(double);
+  if (values_dev && bytes) CUDA_TRY(h, cudaMemcpyAsync(values_dev, h->tg_values, bytes, cudaMemcpyDeviceToDevice, s));
+  if (next_switch_dev && bytes)
+    CUDA_TRY(h, cudaMemcpyAsync(next_switch_dev, h->tg_next, bytes, cudaMemcpyDeviceToDevice, s));
+  if ((times_host || switches_host) && h->tg_count) {
+    std::vector<TelegraphGen> gens(h->tg_count);
+    CUDA_TRY(h, cudaMemcpyAsync(gens.data(), h->tg_gen, h->tg_count * sizeof(TelegraphGen), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < h->tg_count; ++i) {
+      if (times_host) times_host[i] = gens[i].time;
+      if (switches_host) switches_host[i] = gens[i].switches;
+    }
+  }
   return CTQW_OK;
 }
 
@@ -514,12 +628,18 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   // a pinned streaming family (CTQW_STREAM) bypasses the resident path
   if (h->stream_kind == 0 && resident_supported(h->m, h->n, sc)) {
     h->stream_kernel = "resident_kernel";
-    timing_event(h, s);
-    CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step, n_steps,
-                                h->stats, h->events, h->fail, s));
-    timing_event(h, s);
-    h->timed_launches += h->timing ? 1 : 0;
-    h->launches += 1;
+    // dynamic noise changes the couplings after every step: one step per launch
+    const int64_t chunk = h->tg_enabled ? 1 : n_steps;
+    for (int64_t j = 0; j < n_steps; j += chunk) {
+      timing_event(h, s);
+      CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step + j, chunk,
+                                  h->stats, h->events, h->fail, s));
+      timing_event(h, s);
+      h->timed_launches += h->timing ? 1 : 0;
+      h->launches += 1;
+      rc = telegraph_step(h, count, st->dt, s);
+      if (rc) return rc;
+    }
     return CTQW_OK;
   }
   if (!work) return fail_with(h, CTQW_ERR_CONFIG, "work buffer required");
@@ -569,6 +689,8 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       CUDA_TRY(h, launch_norm_decide(h->partial, nparts, count, (long long)(first_step + j + 1), pol,
                                      h->scl, h->stats, h->events, h->fail, s));
       h->launches += 2 * ((count + kMaxGridY - 1) / kMaxGridY);
+      rc = telegraph_step(h, count, st->dt, s);
+      if (rc) return rc;
     }
     double2* final_buf = bufs[n_steps & 1];
     CUDA_TRY(h, launch_rescale(final_buf, count, h->dim, h->scl, s));
@@ -593,6 +715,8 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
     CUDA_TRY(h, launch_norm_decide(h->partial, nparts, count, (long long)(first_step + j + 1), pol,
                                    h->scl, h->stats, h->events, h->fail, s));
     h->launches += 1;
+    rc = telegraph_step(h, count, st->dt, s);
+    if (rc) return rc;
   }
   CUDA_TRY(h, launch_rescale(psi, count, h->dim, h->scl, s));
   h->launches += 2;

@@ -36,6 +36,22 @@ cudaError_t launch_build_coef(const double* noise, int64_t count, int n, int64_t
 cudaError_t launch_fill_states(double2* psi, int64_t count, int64_t dim, const double2* psi0,
                                cudaStream_t s);
 
+// telegraph.cu (dynamic noise, rate > 0)
+struct TelegraphGen {
+  uint64_t state_lo, state_hi, inc_lo, inc_hi;  // PCG64 of the realization's Generator
+  double time;                                   // NoiseProcess.time
+  long long switches;                            // NoiseProcess.switch_count
+};
+cudaError_t launch_telegraph_init(uint64_t master_seed, int64_t r0, int64_t count, const double* levels_dev,
+                                  int n_levels, int64_t total, double mean_wait, double* values,
+                                  double* next_switch, TelegraphGen* gen, cudaStream_t s);
+size_t telegraph_advance_smem(int64_t total);
+cudaError_t launch_telegraph_advance(int64_t count, int64_t total, int64_t n_links, int64_t n_sites, int n,
+                                     double dt, const double* levels_dev, int n_levels, double mean_wait,
+                                     double t_hop, double* values, double* next_switch, TelegraphGen* gen,
+                                     double* hop, double* site, int64_t coef_stride, const long long* fail,
+                                     cudaStream_t s);
+
 // stencil_generic.cu
 cudaError_t launch_apply(int m, const double2* psi, double2* out, int64_t count, int64_t dim,
                          int n, const Coef& coef, const StencilConst& k, bool exact,

@@ -7,90 +7,13 @@
 // pool), PCG64 (128-bit LCG, XSL-RR output) and Generator.integers' buffered
 // 32-bit Lemire bounded draw, so the values are bit-identical to NumPy's.
 #include "ctqw_device.cuh"
+#include "numpy_rng.cuh"
 
 namespace ctqw {
 
 namespace {
 
-constexpr uint32_t kInitA = 0x43b0d7e5u, kMultA = 0x931e8875u;
-constexpr uint32_t kInitB = 0x8b51f9ddu, kMultB = 0x58f38dedu;
-constexpr uint32_t kMixL = 0xca01f9ddu, kMixR = 0x4973f715u;
-constexpr int kXShift = 16;
-
-typedef unsigned __int128 u128;
-
-__device__ __forceinline__ uint32_t hashmix(uint32_t value, uint32_t& hc) {
-  value ^= hc;
-  hc *= kMultA;
-  value *= hc;
-  value ^= value >> kXShift;
-  return value;
-}
-
-__device__ __forceinline__ uint32_t mixw(uint32_t x, uint32_t y) {
-  uint32_t r = kMixL * x - kMixR * y;
-  return r ^ (r >> kXShift);
-}
-
-// Little-endian 32-bit words of v (0 -> one zero word).
-__device__ __forceinline__ int push_words(uint64_t v, uint32_t* w, int n) {
-  if (v == 0) {
-    w[n++] = 0;
-    return n;
-  }
-  while (v) {
-    w[n++] = (uint32_t)(v & 0xffffffffu);
-    v >>= 32;
-  }
-  return n;
-}
-
-struct Pcg64 {
-  u128 state, inc;
-
-  __device__ __forceinline__ void step() {
-    const u128 mult = ((u128)0x2360ed051fc65da4ull << 64) | (u128)0x4385df649fccf645ull;
-    state = state * mult + inc;
-  }
-  __device__ __forceinline__ uint64_t next64() {
-    step();
-    const unsigned rot = (unsigned)(state >> 122);
-    const uint64_t x = (uint64_t)(state >> 64) ^ (uint64_t)state;
-    return (x >> rot) | (x << ((64u - rot) & 63u));
-  }
-};
-
-__device__ void seed_pcg64(uint64_t master_seed, uint64_t r, Pcg64& g) {
-  uint32_t words[4];
-  int nw = push_words(master_seed, words, 0);
-  nw = push_words(r, words, nw);
-  uint32_t pool[4];
-  uint32_t hc = kInitA;
-  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < nw ? words[i] : 0u, hc);
-  for (int s = 0; s < 4; ++s)
-    for (int d = 0; d < 4; ++d)
-      if (s != d) pool[d] = mixw(pool[d], hashmix(pool[s], hc));
-  // (entropy never exceeds the 4-word pool for two 64-bit seed words)
-  uint32_t out32[8];
-  uint32_t hb = kInitB;
-  for (int i = 0; i < 8; ++i) {
-    uint32_t v = pool[i & 3];
-    v ^= hb;
-    hb *= kMultB;
-    v *= hb;
-    v ^= v >> kXShift;
-    out32[i] = v;
-  }
-  uint64_t s64[4];
-  for (int k = 0; k < 4; ++k) s64[k] = (uint64_t)out32[2 * k] | ((uint64_t)out32[2 * k + 1] << 32);
-  const u128 initstate = ((u128)s64[0] << 64) | (u128)s64[1];
-  const u128 initseq = ((u128)s64[2] << 64) | (u128)s64[3];
-  g.state = 0;
-  g.inc = (initseq << 1) | (u128)1;
-  g.step();
-  g.state += initstate;
-  g.step();
-}
+using namespace rng;
 
 __global__ void draw_noise_kernel(uint64_t master_seed, int64_t r0, int64_t count,
                                   const double* __restrict__ levels, int n_levels, int64_t total,

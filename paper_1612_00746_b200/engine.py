@@ -328,15 +328,33 @@ class EnsembleState:
                                  model.ring_tunneling(), model.interaction, model.hbar, device)
         self.dev = torch.device(f"cuda:{device}")
         n = space.lattice.n_sites
-        noise, n_links, n_sites = draw_noise(self.handle, config.noise, config.master_seed, lo,
-                                             self.count)
+        self.dynamic = not config.noise.is_static
+        if self.dynamic:
+            # telegraph process on the device (noise.py:128-206): values and
+            # switch times drawn from the same NumPy-compatible streams, advanced
+            # by ctqw_evolve after every step
+            n_links, n_sites = config.noise.element_counts(n)
+            if config.master_seed < 0 or lo < 0:
+                raise ConfigurationError("seeds must be non-negative")
+            self.handle.telegraph_init(config.master_seed, lo, self.count, config.noise.levels, n_links,
+                                       n_sites, config.noise.rate)
+            noise = None
+        else:
+            noise, n_links, n_sites = draw_noise(self.handle, config.noise, config.master_seed, lo,
+                                                 self.count)
+        self.n_links, self.n_sites = n_links, n_sites
         self.hop = torch.empty((max(self.count, 1), n), dtype=torch.float64, device=self.dev)
         self.site = (torch.empty((max(self.count, 1), n), dtype=torch.float64, device=self.dev)
                      if n_sites else None)
         if self.count:
-            self.handle.build_coefficients(noise.contiguous(), self.count, n_links, n_sites,
-                                           self.hop, self.site)
+            if self.dynamic:
+                self.handle.build_coefficients_from_ptr(self.handle.telegraph_values_ptr(), self.count, n_links,
+                                                        n_sites, self.hop, self.site)
+            else:
+                self.handle.build_coefficients(noise.contiguous(), self.count, n_links, n_sites,
+                                               self.hop, self.site)
         self.handle.bind(self.hop, self.site, self.count, n)
+        self.handle.telegraph_enable(self.dynamic and self.count > 0)
         del noise
         psi0 = build_initial_state(config.initial, space)
         self.psi0 = torch.as_tensor(psi0, device=self.dev)
@@ -365,6 +383,12 @@ class EnsembleState:
             failure = (float(st.fail_deviation), int(st.fail_realization), int(st.fail_step))
         return {"event_count": int(st.event_count), "corrections": int(st.corrections),
                 "max_deviation": float(st.max_deviation), "events": events, "failure": failure}
+
+    def switch_count(self) -> int:
+        """Telegraph switches processed so far in this shard (NoiseProcess.switch_count summed)."""
+        if not self.dynamic or self.count == 0:
+            return 0
+        return int(sum(self.handle.telegraph_read(self.count)[1]))
 
     def diagonal_sum(self, out):
         self.handle.observe_diag(self.psi, self.count, out, accumulate=False)
@@ -491,10 +515,6 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
             raise ConfigurationError(
                 "the eigen backend (dense diagonalisation) is not on the B200 path; use 'taylor' or 'rk4'"
             )
-        if not config.noise.is_static:
-            raise ConfigurationError(
-                "dynamic telegraph noise (rate > 0) is not on the B200 path yet; use rate = 0 (static disorder)"
-            )
         if OBS_PURITY in config.observables:
             work = float(config.realizations) ** 2 * config.space.dim
             if work > PURITY_WORK_CAP:
@@ -538,7 +558,8 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
                 merged = sharding.merge_segment_stats(sharding.gather_objects(local, group))
                 profile.add(STAGE_EVOLUTION, (t_ev - t0) + (clock() - t_obs1),
                             calls=config.realizations * span)
-                # static noise: the Hamiltonian is generated on the fly, nothing to update
+                # the Hamiltonian is generated on the fly; dynamic noise rewrites the
+                # switched couplings inside ctqw_evolve (timed with the evolution)
                 profile.add(STAGE_HAMILTONIAN, 0.0, calls=config.realizations * span)
                 if merged["failure"] is not None:
                     dev, real, step = merged["failure"]
@@ -568,12 +589,14 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
             emit(sinks.observable_rows, rho.time_tag, rows)
             emit(sinks.density_snapshot, rho, target)
 
+    with torch.cuda.device(device):
+        switches = sum(sharding.gather_objects(ens.switch_count(), group))
     report = RunReport(config=config, profile=profile, io_seconds=io_seconds,
                        wall_seconds=clock() - wall_start, workers=world, snapshots=snapshots,
                        max_norm_deviation=max_deviation, norm_corrections=corrections,
-                       norm_events=event_total, switch_count=0, memory_estimate=estimate)
+                       norm_events=event_total, switch_count=switches, memory_estimate=estimate)
     emit(sinks.message,
-         f"run end: snapshots={snapshots} corrections={corrections} switches=0 "
+         f"run end: snapshots={snapshots} corrections={corrections} switches={switches} "
          f"max_norm_deviation={max_deviation:.3e}")
     sinks.finish(report)
     return report

@@ -107,6 +107,12 @@ SIGNATURES = {
     "ctqw_kernel_timing": (ctypes.c_int, [_P, _I32]),
     "ctqw_kernel_time": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
     "ctqw_step_kernel": (ctypes.c_char_p, [_P]),
+    "ctqw_telegraph_init": (ctypes.c_int, [_P, ctypes.c_uint64, _I64, _I64, ctypes.POINTER(_D), _I32, _I64,
+                                           _I64, _D, _P]),
+    "ctqw_telegraph_values": (ctypes.c_void_p, [_P]),
+    "ctqw_telegraph_enable": (ctypes.c_int, [_P, _I32]),
+    "ctqw_telegraph_advance": (ctypes.c_int, [_P, _I64, _D, _P]),
+    "ctqw_telegraph_read": (ctypes.c_int, [_P, _P, _P, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
 }
 
 _lib = None
@@ -219,6 +225,36 @@ class Handle:
         arr = (ctypes.c_double * len(levels))(*[float(v) for v in levels])
         self._check(self.lib.ctqw_draw_noise(self._h, int(master_seed), int(r0), int(count), arr,
                                              len(levels), int(total), _ptr(out), self.stream))
+
+    def telegraph_init(self, master_seed: int, r0: int, count: int, levels, n_links: int, n_sites: int,
+                       rate: float):
+        arr = (ctypes.c_double * len(levels))(*[float(v) for v in levels])
+        self._check(self.lib.ctqw_telegraph_init(self._h, int(master_seed), int(r0), int(count), arr, len(levels),
+                                                 int(n_links), int(n_sites), float(rate), self.stream))
+
+    def telegraph_values_ptr(self) -> int:
+        """Device pointer of the process values ``[count][n_links + n_sites]``."""
+        return int(self.lib.ctqw_telegraph_values(self._h) or 0)
+
+    def telegraph_advance(self, count: int, dt: float):
+        self._check(self.lib.ctqw_telegraph_advance(self._h, int(count), float(dt), self.stream))
+
+    def telegraph_enable(self, enable: bool):
+        self._check(self.lib.ctqw_telegraph_enable(self._h, 1 if enable else 0))
+
+    def telegraph_read(self, count: int, values=None, next_switch=None):
+        """(times, switch counts) per realization; optionally copies values /
+        next switch times into the given ``(count, total)`` device tensors."""
+        times = (ctypes.c_double * max(count, 1))()
+        sw = (ctypes.c_int64 * max(count, 1))()
+        self._check(self.lib.ctqw_telegraph_read(self._h, _ptr(values), _ptr(next_switch), times, sw,
+                                                 self.stream))
+        return [times[i] for i in range(count)], [sw[i] for i in range(count)]
+
+    def build_coefficients_from_ptr(self, noise_ptr: int, count: int, n_links: int, n_sites: int, hop, site):
+        self._check(self.lib.ctqw_build_coefficients(self._h, ctypes.c_void_p(noise_ptr), int(count),
+                                                     int(n_links), int(n_sites), _ptr(hop), _ptr(site),
+                                                     self.stream))
 
     def build_coefficients(self, noise, count: int, n_links: int, n_sites: int, hop, site):
         self._check(self.lib.ctqw_build_coefficients(self._h, _ptr(noise), int(count), int(n_links),

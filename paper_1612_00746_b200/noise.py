@@ -7,8 +7,12 @@ realization on the GPU, so the values equal
 ``np.random.default_rng((master_seed, r)).choice(levels, n_links + n_sites)``
 bit for bit, laid out ``[links (N) | sites (N)]`` per realization.
 
-Dynamic telegraph noise (``rate > 0``, noise.py:165-206) is not on the B200
-path yet; ``run`` rejects it.
+Dynamic telegraph noise (``rate > 0``, noise.py:71-206) runs on the device as
+well (``csrc/telegraph.cu``): ``ctqw_telegraph_init`` draws the values with
+``choice`` and the switch times with ``exponential`` from the same
+per-realization streams (NumPy's ziggurat, bit-compatible), and
+``ctqw_evolve`` advances the process after every step.  ``init_process`` /
+``advance`` below expose one realization's process with the reference's API.
 """
 
 from __future__ import annotations
@@ -96,16 +100,77 @@ class StaticNoise:
         return self.values[self.n_links:]
 
 
-def init_process(spec: NoiseSpec, where, seed) -> StaticNoise:
-    """Static-noise draw for one realization, seed ``(master_seed, r)``.
+@dataclass
+class NoiseDelta:
+    """Report of one advance window (noise.py:71-78)."""
 
-    Same values as the reference's ``init_process`` for ``rate == 0``.
+    changed: bool
+    links: np.ndarray
+    sites: np.ndarray
+    switches: int
+
+
+class TelegraphProcess:
+    """Telegraph state of one realization (the reference's ``NoiseProcess``
+    for ``rate > 0``), held on the device by a one-realization handle."""
+
+    def __init__(self, spec, n_links, n_sites, handle):
+        self.spec = spec
+        self.n_links = n_links
+        self.n_sites = n_sites
+        self._h = handle
+        self._sync()
+
+    def _sync(self):
+        import torch
+
+        total = self.n_links + self.n_sites
+        dev = f"cuda:{self._h.device}"
+        vals = torch.empty((1, max(total, 1)), dtype=torch.float64, device=dev)
+        nxt = torch.empty_like(vals)
+        times, sw = self._h.telegraph_read(1, vals if total else None, nxt if total else None)
+        self.values = vals[0, :total].cpu().numpy()
+        self.next_switch = nxt[0, :total].cpu().numpy()
+        self.time = float(times[0])
+        self.switch_count = int(sw[0])
+
+    @property
+    def link_values(self):
+        return self.values[: self.n_links]
+
+    @property
+    def site_values(self):
+        return self.values[self.n_links:]
+
+
+def advance(process, dt: float) -> NoiseDelta:
+    """Advance over ``(time, time + dt]`` (noise.py:165-206); a static process
+    only moves its clock."""
+    if dt < 0:
+        raise ConfigurationError(f"advance window dt = {dt} must be >= 0")
+    empty = np.empty(0, dtype=np.int64)
+    if isinstance(process, StaticNoise):
+        process.time += dt
+        return NoiseDelta(False, empty, empty, 0)
+    before = process.values.copy()
+    switches0 = process.switch_count
+    process._h.telegraph_advance(1, dt)
+    process._sync()
+    changed = process.values != before
+    links = np.nonzero(changed[: process.n_links])[0]
+    sites = np.nonzero(changed[process.n_links:])[0]
+    return NoiseDelta(bool(links.size or sites.size), links, sites, process.switch_count - switches0)
+
+
+def init_process(spec: NoiseSpec, where, seed):
+    """Noise draw for one realization, seed ``(master_seed, r)``.
+
+    Same values (and, for ``rate > 0``, switch times) as the reference's
+    ``init_process``.
     """
     from .hamiltonian import handle_for
     from .geometry import JointSpace, LatticeTopology, RingStencil
 
-    if not spec.is_static:
-        raise ConfigurationError("dynamic noise (rate > 0) is not on the B200 path")
     if isinstance(where, RingStencil):
         lattice = where.space.lattice
     elif isinstance(where, JointSpace):
@@ -116,7 +181,28 @@ def init_process(spec: NoiseSpec, where, seed) -> StaticNoise:
         raise ConfigurationError(f"cannot take a lattice from {type(where).__name__}")
     if not (isinstance(seed, (tuple, list)) and len(seed) == 2):
         raise ConfigurationError("the device draw takes seeds of the form (master_seed, r)")
-    handle = handle_for(1, max(lattice.n_sites, 3), 0.0, 1.0, 0.0, 1.0)
     counts = spec.element_counts(lattice.n_sites, lattice.moves_half)
+    if int(seed[0]) < 0 or int(seed[1]) < 0:
+        raise ConfigurationError("seeds must be non-negative")
+    if not spec.is_static:
+        from .native import Handle
+
+        n = max(lattice.n_sites, 3)
+        if counts[0] not in (0, n) or counts[1] not in (0, n):
+            raise ConfigurationError("the device telegraph process needs a ring (K = 1) lattice")
+        handle = Handle(1, n, 0.0, 1.0, 0.0, 1.0, _device())
+        handle.telegraph_init(int(seed[0]), int(seed[1]), 1, spec.levels, counts[0], counts[1], spec.rate)
+        return TelegraphProcess(spec, counts[0], counts[1], handle)
+    handle = handle_for(1, max(lattice.n_sites, 3), 0.0, 1.0, 0.0, 1.0)
     vals, nl, ns = draw_noise(handle, spec, int(seed[0]), int(seed[1]), 1, counts)
     return StaticNoise(spec, nl, ns, vals[0].cpu().numpy())
+
+
+def _device() -> int:
+    import torch
+
+    if not torch.cuda.is_available():
+        from .errors import NativeError
+
+        raise NativeError("no CUDA device: the B200 path has no CPU fallback")
+    return torch.cuda.current_device()

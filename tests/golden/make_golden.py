@@ -193,11 +193,64 @@ def run_fixture():
     np.savez_compressed(os.path.join(HERE, "run_rows.npz"), meta=json.dumps(meta), **arrays)
 
 
+def telegraph_fixture():
+    """Reference dynamic (telegraph) noise: process states after k advances
+    (noise.py:128-206) and ``run()`` rows/switch counts with rate > 0."""
+    from ctqw.noise import advance
+
+    arrays = {}
+    meta = {"trajectories": [], "runs": []}
+    traj = (
+        dict(n=12, target="both", levels=(-0.1, 0.1, 0.3), rate=0.7, seed=1234, r0=5, count=3, dt=0.05,
+             checkpoints=(0, 1, 7, 40)),
+        dict(n=20, target="tunneling", levels=(-0.2, 0.2), rate=2.5, seed=99, r0=0, count=2, dt=0.13,
+             checkpoints=(3, 25)),
+    )
+    for ti, c in enumerate(traj):
+        spec = NoiseSpec(target=c["target"], levels=c["levels"], rate=c["rate"])
+        lat = build_lattice([c["n"]])
+        procs = [init_process(spec, lat, seed=(c["seed"], r)) for r in range(c["r0"], c["r0"] + c["count"])]
+        done = 0
+        for k in c["checkpoints"]:
+            for _ in range(k - done):
+                for pr in procs:
+                    advance(pr, c["dt"])
+            done = k
+            arrays[f"traj{ti}_values_{k}"] = np.stack([pr.values for pr in procs])
+            arrays[f"traj{ti}_next_{k}"] = np.stack([pr.next_switch for pr in procs])
+            arrays[f"traj{ti}_time_{k}"] = np.array([pr.time for pr in procs])
+            arrays[f"traj{ti}_switches_{k}"] = np.array([pr.switch_count for pr in procs])
+        meta["trajectories"].append(dict(c, n_links=procs[0].n_links, n_sites=procs[0].n_sites))
+    runs = (
+        dict(n=10, m=2, R=5, steps=40, post_rate=10, backend="taylor", dt=0.05, target="both", rate=0.8),
+        dict(n=9, m=2, R=4, steps=30, post_rate=15, backend="rk4", dt=0.05, target="tunneling", rate=2.0),
+    )
+    for idx, c in enumerate(runs):
+        space = JointSpace(lattice=build_lattice([c["n"]]), m=c["m"])
+        cfg = RunConfig(
+            space=space,
+            model=CouplingModel(onsite_energy=0.1, tunneling=1.0, interaction=0.5),
+            noise=NoiseSpec(target=c["target"], levels=(-0.1, 0.1), rate=c["rate"]),
+            stepper=StepperConfig(backend=c["backend"], dt=c["dt"]),
+            realizations=c["R"], steps=c["steps"], post_rate=c["post_rate"],
+            master_seed=1234, workers=1, precision="double",
+        )
+        sinks = MemorySinks()
+        report = run(cfg, sinks)
+        arrays[f"run{idx}_rows"] = np.array([r[3] for r in sinks.rows], dtype=np.float64)
+        meta["runs"].append(dict(c, rows=[(r[0], r[1], r[2]) for r in sinks.rows], onsite=0.1, tunneling=1.0,
+                                 interaction=0.5, switch_count=report.switch_count,
+                                 corrections=report.norm_corrections, norm_events=report.norm_events))
+    np.savez_compressed(os.path.join(HERE, "telegraph.npz"), meta=json.dumps(meta), **arrays)
+
+
 if __name__ == "__main__":
-    noise_fixture()
-    stencil_fixture()
-    segment_fixture()
-    run_fixture()
+    import sys as _sys
+
+    only = _sys.argv[1:]
+    for fn in (noise_fixture, stencil_fixture, segment_fixture, run_fixture, telegraph_fixture):
+        if not only or fn.__name__ in only:
+            fn()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -492,3 +492,130 @@ def test_streaming_kernels_bitwise_repeatable(pkg, monkeypatch, m, n, B, family)
         for _ in range(3):
             again, _ = run_evolve(h, psi0, B, 3, stepper("taylor", 4, dt, exact=exact))
             np.testing.assert_array_equal(first, again)
+
+
+# ---------------------------------------------------------------------------
+# dynamic telegraph noise (rate > 0): device process vs the reference
+
+
+@pytest.mark.parametrize("ti", range(2))
+def test_telegraph_device_process_matches_reference(pkg, ti):
+    """Device NoiseProcess (init + advance inside ctqw_evolve) == the
+    reference's init_process/advance: values, times, switch counts exact;
+    switch times exact up to the rare exp/log1p slow paths (<= 2 ulp)."""
+    data, meta = load_golden("telegraph.npz")
+    c = meta["trajectories"][ti]
+    n, B = c["n"], c["count"]
+    h = make_handle(1, n)
+    dev = torch.device("cuda:0")
+    h.telegraph_init(c["seed"], c["r0"], B, c["levels"], c["n_links"], c["n_sites"], c["rate"])
+    hop = torch.empty((B, n), dtype=torch.float64, device=dev)
+    site = torch.empty((B, n), dtype=torch.float64, device=dev) if c["n_sites"] else None
+    h.build_coefficients_from_ptr(h.telegraph_values_ptr(), B, c["n_links"], c["n_sites"], hop, site)
+    h.bind(hop, site, B, n)
+    h.telegraph_enable(True)
+    total = c["n_links"] + c["n_sites"]
+    psi = to_dev(np.tile(orc.product_state(1, n), (B, 1)))
+    work = torch.empty_like(psi)
+    done = 0
+    for k in c["checkpoints"]:
+        if k > done:
+            if h.evolve(psi, work, B, done, k - done, stepper(dt=c["dt"], tol_fail=0.5)):
+                psi, work = work, psi
+        done = k
+        vals = torch.empty((B, total), dtype=torch.float64, device=dev)
+        nxt = torch.empty_like(vals)
+        times, sw = h.telegraph_read(B, vals, nxt)
+        np.testing.assert_array_equal(vals.cpu().numpy(), data[f"traj{ti}_values_{k}"])
+        np.testing.assert_array_equal(np.array(times), data[f"traj{ti}_time_{k}"])
+        np.testing.assert_array_equal(np.array(sw), data[f"traj{ti}_switches_{k}"])
+        ref = data[f"traj{ti}_next_{k}"]
+        mine = nxt.cpu().numpy()
+        assert np.all(np.abs(mine - ref) <= 2 * np.spacing(np.abs(ref)))
+        # the couplings are a fresh assembly of the current values (hamiltonian.py:131-141)
+        if c["n_links"]:
+            np.testing.assert_array_equal(hop.cpu().numpy(), 1.0 + data[f"traj{ti}_values_{k}"][:, : c["n_links"]])
+
+
+@pytest.mark.parametrize("idx", range(2))
+def test_run_dynamic_noise_matches_reference(pkg, idx):
+    p = pkg
+    data, meta = load_golden("telegraph.npz")
+    c = meta["runs"][idx]
+    cfg = p.RunConfig(
+        space=p.JointSpace(p.build_lattice([c["n"]]), c["m"]),
+        model=p.CouplingModel(onsite_energy=c["onsite"], tunneling=c["tunneling"], interaction=c["interaction"]),
+        noise=p.NoiseSpec(target=c["target"], levels=(-0.1, 0.1), rate=c["rate"]),
+        stepper=p.StepperConfig(backend=c["backend"], dt=c["dt"]),
+        realizations=c["R"], steps=c["steps"], post_rate=c["post_rate"], master_seed=1234, precision="double",
+    )
+    sinks = p.MemorySinks()
+    report = p.run(cfg, sinks)
+    assert [(t, n, i) for t, n, i, _ in sinks.rows] == [tuple(r) for r in c["rows"]]
+    np.testing.assert_allclose([v for *_, v in sinks.rows], data[f"run{idx}_rows"], rtol=1e-10, atol=1e-13)
+    assert report.switch_count == c["switch_count"]
+    assert report.norm_corrections == c["corrections"]
+
+
+DYN_CASES = [
+    # (m, n, B, backend, dt, steps, target, family)
+    (2, 40, 3, "taylor", 0.05, 12, "both", None),        # resident, one step per launch
+    (2, 96, 4, "taylor", 0.04, 8, "both", "band4"),
+    (2, 256, 2, "rk4", 0.03, 5, "tunneling", "band4"),
+    (2, 100, 2, "taylor", 0.04, 6, "onsite", "band"),
+    (3, 12, 2, "taylor", 0.04, 6, "both", None),         # generic
+    (3, 128, 1, "taylor", 0.03, 3, "both", None),        # plane3
+]
+
+
+@pytest.mark.parametrize("case", DYN_CASES, ids=[f"m{c[0]}n{c[1]}{c[3]}{c[7] or 'auto'}" for c in DYN_CASES])
+def test_dynamic_noise_every_kernel_matches_oracle(pkg, monkeypatch, case):
+    """Couplings rewritten after every step, on every step-kernel family."""
+    from oracle.noise_oracle import TelegraphOracle
+
+    m, n, B, backend, dt, steps, target, family = case
+    if family:
+        monkeypatch.setenv("CTQW_STREAM", family)
+    rate, levels, seed = 3.0, (-0.1, 0.1), 77
+    nl = n if target in ("tunneling", "both") else 0
+    ns = n if target in ("onsite", "both") else 0
+    h = make_handle(m, n, 0.2, 1.0, 0.7, 1.0)
+    dev = torch.device("cuda:0")
+    h.telegraph_init(seed, 0, B, levels, nl, ns, rate)
+    hop = torch.empty((B, n), dtype=torch.float64, device=dev)
+    site = torch.empty((B, n), dtype=torch.float64, device=dev) if ns else None
+    h.build_coefficients_from_ptr(h.telegraph_values_ptr(), B, nl, ns, hop, site)
+    h.bind(hop, site, B, n)
+    h.telegraph_enable(True)
+    psi0 = np.tile(orc.product_state(m, n), (B, 1))
+    mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, 4, dt))
+    tg = TelegraphOracle(seed, 0, B, levels, nl, ns, rate)
+    st = orc.make_stencil(m, n, 0.2, 1.0, 0.7, link=tg.link_values() if nl else None,
+                          site=tg.site_values().copy() if ns else None, batch=B)
+    ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, 4, noise=tg, tunneling=1.0)
+    assert int(tg.switches.sum()) > 0
+    assert_stats_match(stats, ostats)
+    if ostats.event_count == 0:
+        np.testing.assert_array_equal(mine, ref)
+    else:
+        assert np.abs(mine - ref).max() <= 1e-13
+
+
+def test_init_process_advance_api_matches_reference(pkg):
+    """The reference-facing per-realization API (init_process / advance)."""
+    p = pkg
+    data, meta = load_golden("telegraph.npz")
+    c = meta["trajectories"][0]
+    spec = p.NoiseSpec(target=c["target"], levels=c["levels"], rate=c["rate"])
+    lat = p.build_lattice([c["n"]])
+    procs = [p.init_process(spec, lat, seed=(c["seed"], r)) for r in range(c["r0"], c["r0"] + c["count"])]
+    done, switched = 0, 0
+    for k in c["checkpoints"]:
+        for _ in range(k - done):
+            for pr in procs:
+                d = p.advance(pr, c["dt"])
+                switched += d.switches
+        done = k
+        np.testing.assert_array_equal(np.stack([pr.values for pr in procs]), data[f"traj0_values_{k}"])
+        np.testing.assert_array_equal([pr.switch_count for pr in procs], data[f"traj0_switches_{k}"])
+    assert switched == int(data[f"traj0_switches_{c['checkpoints'][-1]}"].sum())

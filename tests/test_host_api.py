@@ -131,8 +131,6 @@ def test_run_rejects_out_of_scope_before_touching_device():
         p.run(cfg(memory_budget=16))
     with pytest.raises(p.ConfigurationError):
         p.run(cfg(stepper=p.StepperConfig(backend="eigen")))
-    with pytest.raises(p.ConfigurationError):
-        p.run(cfg(noise=p.NoiseSpec(rate=0.5)))
     with pytest.raises(p.CapacityError):
         p.run(cfg(space=ring(1024, 2), realizations=10000, memory_budget=2**50))
 
@@ -146,6 +144,8 @@ def test_no_cpu_fallback():
         p.run(cfg())
     with pytest.raises(p.NativeError):
         native.Handle(2, 16, 0.0, 1.0, 0.0, 1.0)
+    with pytest.raises(p.NativeError):
+        p.run(cfg(noise=p.NoiseSpec(rate=0.5)))  # dynamic noise is device-only too
 
 
 def test_library_exports_every_declared_symbol():

@@ -116,3 +116,48 @@ def test_run_rows(idx):
     np.testing.assert_allclose(mine, ref, rtol=1e-10, atol=1e-13)
     assert totals.corrections == c["corrections"]
     assert totals.event_count == c["norm_events"]
+
+
+# ---------------------------------------------------------------------------
+# dynamic telegraph noise (rate > 0)
+
+
+@pytest.mark.parametrize("ti", range(2))
+def test_telegraph_oracle_matches_reference_trajectory(ti):
+    """TelegraphOracle == the reference's init_process/advance, bit for bit."""
+    from oracle.noise_oracle import TelegraphOracle
+
+    data, meta = load_golden("telegraph.npz")
+    c = meta["trajectories"][ti]
+    tg = TelegraphOracle(c["seed"], c["r0"], c["count"], c["levels"], c["n_links"], c["n_sites"], c["rate"])
+    done = 0
+    for k in c["checkpoints"]:
+        for _ in range(k - done):
+            tg.advance(c["dt"])
+        done = k
+        np.testing.assert_array_equal(tg.values, data[f"traj{ti}_values_{k}"])
+        np.testing.assert_array_equal(tg.next_switch, data[f"traj{ti}_next_{k}"])
+        np.testing.assert_array_equal(tg.time, data[f"traj{ti}_time_{k}"])
+        np.testing.assert_array_equal(tg.switches, data[f"traj{ti}_switches_{k}"])
+
+
+@pytest.mark.parametrize("idx", range(2))
+def test_run_rows_dynamic_noise(idx):
+    """Oracle run with telegraph noise == the reference's run() rows."""
+    from oracle.noise_oracle import TelegraphOracle
+
+    data, meta = load_golden("telegraph.npz")
+    c = meta["runs"][idx]
+    nl = c["n"] if c["target"] in ("tunneling", "both") else 0
+    ns = c["n"] if c["target"] in ("onsite", "both") else 0
+    tg = TelegraphOracle(1234, 0, c["R"], (-0.1, 0.1), nl, ns, c["rate"])
+    st = orc.make_stencil(c["m"], c["n"], c["onsite"], c["tunneling"], c["interaction"],
+                          link=tg.link_values() if nl else None, site=tg.site_values().copy() if ns else None,
+                          batch=c["R"])
+    out, _, totals = orc.run_rows(st, orc.product_state(c["m"], c["n"]), c["R"], c["steps"], c["post_rate"],
+                                  c["dt"], backend=c["backend"], noise=tg, tunneling=c["tunneling"])
+    rows = [(t, name, i, v) for t, rr in out for name, i, v in rr]
+    assert [(t, n, i) for t, n, i, _ in rows] == [tuple(r) for r in c["rows"]]
+    np.testing.assert_allclose([v for *_, v in rows], data[f"run{idx}_rows"], rtol=1e-10, atol=1e-13)
+    assert int(tg.switches.sum()) == c["switch_count"]
+    assert totals.corrections == c["corrections"]
