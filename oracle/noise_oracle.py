@@ -22,9 +22,12 @@ The arithmetic lives in NumPy (third-party, not vendored under
   ``generate_state(4, uint64)`` (numpy/random/src/pcg64/pcg64.{h,c});
 * ``Generator.choice(a, size)`` with ``replace=True, p=None`` =
   ``integers(0, len(a), size, dtype=int64)`` -> ``random_bounded_uint64_fill``
-  -> 32-bit buffered Lemire rejection (numpy/random/src/distributions/
-  distributions.c: ``buffered_bounded_lemire_uint32``), consuming the low
-  half of each 64-bit output first, then the cached high half.
+  -> 32-bit Lemire rejection on ``next_uint32`` (numpy/random/src/
+  distributions/distributions.c: ``buffered_bounded_lemire_uint32``), which
+  for PCG64 hands out the low half of each 64-bit output first, then the high
+  half cached in the bit generator.  The cache persists across calls; for the
+  static draw (one call on a fresh generator) ``bounded_indices`` below
+  models it locally.
 
 Pinned by ``tests/test_oracle_golden.py`` against draws produced by the
 reference's own ``init_process`` (fixtures in ``tests/golden/``).

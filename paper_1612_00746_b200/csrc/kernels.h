@@ -39,6 +39,8 @@ cudaError_t launch_fill_states(double2* psi, int64_t count, int64_t dim, const d
 // telegraph.cu (dynamic noise, rate > 0)
 struct TelegraphGen {
   uint64_t state_lo, state_hi, inc_lo, inc_hi;  // PCG64 of the realization's Generator
+  uint32_t u32;                                  // PCG64's cached upper half (next_uint32)
+  int has_u32;
   double time;                                   // NoiseProcess.time
   long long switches;                            // NoiseProcess.switch_count
 };

@@ -27,39 +27,9 @@ __global__ void draw_noise_kernel(uint64_t master_seed, int64_t r0, int64_t coun
   }
   Pcg64 g;
   seed_pcg64(master_seed, (uint64_t)(r0 + i), g);
-  const uint32_t rng = (uint32_t)(n_levels - 1);
-  const uint32_t excl = rng + 1u;
-  const uint32_t threshold = (0xffffffffu - rng) % excl;
-  uint64_t buf = 0;
-  int have = 0;
-  for (int64_t k = 0; k < total; ++k) {
-    uint32_t u;
-    if (!have) {
-      buf = g.next64();
-      have = 1;
-      u = (uint32_t)buf;
-    } else {
-      have = 0;
-      u = (uint32_t)(buf >> 32);
-    }
-    uint64_t m = (uint64_t)u * excl;
-    uint32_t leftover = (uint32_t)m;
-    if (leftover < excl) {
-      while (leftover < threshold) {
-        if (!have) {
-          buf = g.next64();
-          have = 1;
-          u = (uint32_t)buf;
-        } else {
-          have = 0;
-          u = (uint32_t)(buf >> 32);
-        }
-        m = (uint64_t)u * excl;
-        leftover = (uint32_t)m;
-      }
-    }
-    row[k] = levels[m >> 32];
-  }
+  const Bounded32 b((uint32_t)(n_levels - 1));
+  U32Cache c{0u, 0};  // a fresh generator has no cached half
+  for (int64_t k = 0; k < total; ++k) row[k] = levels[b.draw(g, c)];
 }
 
 // hop = t + xi_link (hamiltonian.py:137-141: out[...,1:] = base; += link),

@@ -94,30 +94,37 @@ __device__ __forceinline__ void seed_pcg64(uint64_t master_seed, uint64_t r, Pcg
   g.step();
 }
 
-// Generator.integers(0, rng + 1) for one call of ``size`` draws: the 32-bit
-// buffer (low half of a 64-bit output first, then the cached high half) is
-// local to the call, as in random_bounded_uint64_fill.
+// Generator.integers(0, rng + 1) / choice: 32-bit Lemire with rejection on
+// next_uint32.  PCG64's next_uint32 hands out the low half of a 64-bit output
+// and caches the high half in the bit generator (has_uint32 / uinteger in
+// numpy/random/src/pcg64/pcg64.h), so the cache persists across calls and is
+// untouched by next_uint64 draws (exponential); callers keep it with the state.
+struct U32Cache {
+  uint32_t value;
+  int has;
+};
+
+__device__ __forceinline__ uint32_t next_u32(Pcg64& g, U32Cache& c) {
+  if (c.has) {
+    c.has = 0;
+    return c.value;
+  }
+  const uint64_t next = g.next64();
+  c.has = 1;
+  c.value = (uint32_t)(next >> 32);
+  return (uint32_t)next;
+}
+
 struct Bounded32 {
   uint32_t rng, excl, threshold;
-  uint64_t buf;
-  int have;
   __device__ __forceinline__ explicit Bounded32(uint32_t r)
-      : rng(r), excl(r + 1u), threshold((0xffffffffu - r) % (r + 1u)), buf(0), have(0) {}
-  __device__ __forceinline__ uint32_t next32(Pcg64& g) {
-    if (!have) {
-      buf = g.next64();
-      have = 1;
-      return (uint32_t)buf;
-    }
-    have = 0;
-    return (uint32_t)(buf >> 32);
-  }
-  __device__ __forceinline__ uint32_t draw(Pcg64& g) {
-    uint64_t m = (uint64_t)next32(g) * excl;
+      : rng(r), excl(r + 1u), threshold((0xffffffffu - r) % (r + 1u)) {}
+  __device__ __forceinline__ uint32_t draw(Pcg64& g, U32Cache& c) const {
+    uint64_t m = (uint64_t)next_u32(g, c) * excl;
     uint32_t leftover = (uint32_t)m;
     if (leftover < excl) {
       while (leftover < threshold) {
-        m = (uint64_t)next32(g) * excl;
+        m = (uint64_t)next_u32(g, c) * excl;
         leftover = (uint32_t)m;
       }
     }

@@ -40,11 +40,12 @@ __global__ void telegraph_init_kernel(uint64_t master_seed, int64_t r0, int64_t 
   seed_pcg64(master_seed, (uint64_t)(r0 + i), g);
   double* v = values + i * total;
   double* ns = next_switch + i * total;
+  U32Cache c{0u, 0};
   if (n_levels == 1) {
     for (int64_t k = 0; k < total; ++k) v[k] = levels[0];
   } else {
-    Bounded32 b((uint32_t)(n_levels - 1));
-    for (int64_t k = 0; k < total; ++k) v[k] = levels[b.draw(g)];
+    const Bounded32 b((uint32_t)(n_levels - 1));
+    for (int64_t k = 0; k < total; ++k) v[k] = levels[b.draw(g, c)];
   }
   for (int64_t k = 0; k < total; ++k) ns[k] = __dmul_rn(mean_wait, standard_exponential(g));
   TelegraphGen t;
@@ -52,6 +53,8 @@ __global__ void telegraph_init_kernel(uint64_t master_seed, int64_t r0, int64_t 
   t.state_hi = (uint64_t)(g.state >> 64);
   t.inc_lo = (uint64_t)g.inc;
   t.inc_hi = (uint64_t)(g.inc >> 64);
+  t.u32 = c.value;
+  t.has_u32 = c.has;
   t.time = 0.0;
   t.switches = 0;
   gen[i] = t;
@@ -97,14 +100,15 @@ __global__ void __launch_bounds__(32 * kAdvWarps) telegraph_advance_kernel(
     Pcg64 g;
     g.state = ((u128)t.state_hi << 64) | (u128)t.state_lo;
     g.inc = ((u128)t.inc_hi << 64) | (u128)t.inc_lo;
+    U32Cache c{t.u32, t.has_u32};
     long long switches = 0;
     while (k > 0) {
       switches += k;
       if (n_levels == 1) {
         for (int q = 0; q < k; ++q) v[cur[q]] = levels[0];
       } else {
-        Bounded32 b((uint32_t)(n_levels - 1));  // one choice() call
-        for (int q = 0; q < k; ++q) v[cur[q]] = levels[b.draw(g)];
+        const Bounded32 b((uint32_t)(n_levels - 1));  // one choice() call
+        for (int q = 0; q < k; ++q) v[cur[q]] = levels[b.draw(g, c)];
       }
       for (int q = 0; q < k; ++q) {  // one exponential() call, then the in-place add
         const int e = cur[q];
@@ -117,6 +121,8 @@ __global__ void __launch_bounds__(32 * kAdvWarps) telegraph_advance_kernel(
     }
     t.state_lo = (uint64_t)g.state;
     t.state_hi = (uint64_t)(g.state >> 64);
+    t.u32 = c.value;
+    t.has_u32 = c.has;
     t.switches += switches;
   }
   __syncwarp();
