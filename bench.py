@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--backend", default="taylor", choices=("taylor", "rk4"))
     ap.add_argument("--order", type=int, default=4)
     ap.add_argument("--dt", type=float, default=0.02)
+    ap.add_argument("--rate", type=float, default=0.0,
+                    help="telegraph switching rate (0 = static disorder, the BASELINE configs; the "
+                         "reference's CLI default is 0.1)")
     ap.add_argument("--exact", action="store_true",
                     help="reference operation order without FMA (bit-identical to the reference between "
                          "renormalisations) for the headline value; default is the FMA-contracted stencil, "
@@ -306,7 +309,7 @@ def ours(a):
     R_total = a.realizations * world
     obs = ("populations", "position_mean_variance", "participation_ratio")
     cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([a.n]), a.m),
-                      noise=p.NoiseSpec(target="tunneling", levels=(-0.1, 0.1), rate=0.0),
+                      noise=p.NoiseSpec(target="tunneling", levels=(-0.1, 0.1), rate=a.rate),
                       stepper=p.StepperConfig(backend=a.backend, dt=a.dt, taylor_order=a.order),
                       realizations=R_total, steps=a.steps, post_rate=a.steps, precision="double",
                       observables=obs, memory_budget=170 * 2**30, exact=bool(a.exact), device=local)

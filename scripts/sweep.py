@@ -43,7 +43,7 @@ def timed(ens, cfg, steps, post_rate, engine, torch):
     return start.elapsed_time(stop) / 1000.0
 
 
-def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling", post_rates=(None,),
+def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling", post_rates=(None,), rate=0.0,
              observables=("populations", "position_mean_variance", "participation_ratio")):
     import torch
 
@@ -51,7 +51,7 @@ def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling"
     from paper_1612_00746_b200 import engine
 
     cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([n]), m),
-                      noise=p.NoiseSpec(target=target, levels=(-0.1, 0.1), rate=0.0),
+                      noise=p.NoiseSpec(target=target, levels=(-0.1, 0.1), rate=rate),
                       stepper=p.StepperConfig(backend=backend, dt=dt), realizations=R, steps=steps,
                       post_rate=steps, precision="double", observables=observables,
                       memory_budget=175 * 2**30, exact=False, device=0)
@@ -66,11 +66,11 @@ def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling"
         for pr in post_rates:
             prate = steps if pr is None else pr
             secs = timed(ens, cfg, steps, prate, engine, torch)
-            rate = R * steps / secs
+            thr = R * steps / secs
             line = {"case": name, "m": m, "n": n, "realizations": R, "steps": steps, "backend": backend,
-                    "post_rate": prate, "exact": ex, "seconds": secs, "r_steps_per_s": rate,
+                    "post_rate": prate, "exact": ex, "seconds": secs, "r_steps_per_s": thr, "noise_rate": cfg.noise.rate,
                     "kernel": ens.handle.step_kernel(),
-                    "hbm_frac_of_measured": rate * 32.0 * n ** m / PEAK}
+                    "hbm_frac_of_measured": thr * 32.0 * n ** m / PEAK}
             print(json.dumps(line), flush=True)
             out.append(line)
     del ens
@@ -95,6 +95,8 @@ def main():
     # configs[3]: N=512, post-processing frequency sweep
     run_case("configs[3] N=512 R=1000 post sweep", 2, 512, 1000, 100 if q else 1000,
              post_rates=(1, 10, 100, None) if not q else (1, 10, None))
+    # the reference's CLI default noise: dynamic telegraph switching at rate 0.1
+    run_case("configs[1] N=256 R=1000 telegraph rate=0.1", 2, 256, 1000, 50 if q else 200, rate=0.1)
     # configs[4]: m=3, N=128 (D=2^21), 16-CTA cluster kernel; the largest ensemble that fits
     # (two 32 MiB buffers per realization) is ~2600 per GPU -- R=2048 here
     run_case("configs[4] m=3 N=128 R=2048", 3, 128, 2048, 5 if q else 20, dt=0.015)
