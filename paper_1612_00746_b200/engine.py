@@ -252,8 +252,13 @@ class OutputSinks:
 
 
 class MemorySinks(OutputSinks):
-    def __init__(self, keep_densities: bool = True, max_events: int = 1000):
+    """The reference's MemorySinks (ensemble.py:345-373).  ``dense=True`` asks
+    ``run`` for the dense packed <rho> (``density.DensityMatrix``) at every
+    collection point instead of its diagonal (``DiagonalDensity``)."""
+
+    def __init__(self, keep_densities: bool = True, max_events: int = 1000, dense: bool = False):
         self.keep_densities = keep_densities
+        self.dense_density = bool(dense) and keep_densities
         self.max_events = max_events
         self.rows = []
         self.densities = []
@@ -415,6 +420,28 @@ def _observable_rows(config, pops, pr, purity, joint):
         elif name == OBS_JOINT:
             rows.extend(("joint_probability", i, float(v)) for i, v in enumerate(joint))
     return rows
+
+
+def _dense_snapshot(config, ens, group, time_tag):
+    """Packed <rho> over all ranks (density.py:91-96): each rank's Gram sum of
+    its shard, all-reduced, divided by R."""
+    import torch
+
+    from .density import DensityMatrix, packed_density_device, packed_length
+
+    dim = config.space.dim
+    if ens.count:
+        part = packed_density_device(ens.states(), ens.count) * ens.count
+    else:
+        part = torch.zeros(packed_length(dim), dtype=torch.complex128, device=ens.dev)
+    if group is not None and sharding.world_info(group)[1] > 1:
+        import torch.distributed as dist
+
+        real = torch.view_as_real(part).contiguous()
+        dist.all_reduce(real, group=group)
+        part = torch.view_as_complex(real)
+    return DensityMatrix(None, dim=dim, sample_count=config.realizations, time_tag=float(time_tag),
+                         device_packed=part / config.realizations)
 
 
 class PendingObservables:
@@ -581,10 +608,13 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
                 joint = pending.joint() if OBS_JOINT in config.observables else None
                 time_tag = target * config.stepper.dt
                 rows = _observable_rows(config, pops, pending.participation_ratio, pending.purity, joint)
-                rho = DiagonalDensity(diag=None, dim=config.space.dim, sample_count=config.realizations,
-                                      time_tag=float(time_tag), purity=pending.purity, populations=pops,
-                                      participation_ratio=pending.participation_ratio,
-                                      device_diag=pending.diag_dev)
+                if getattr(sinks, "dense_density", False):
+                    rho = _dense_snapshot(config, ens, group, time_tag)
+                else:
+                    rho = DiagonalDensity(diag=None, dim=config.space.dim, sample_count=config.realizations,
+                                          time_tag=float(time_tag), purity=pending.purity, populations=pops,
+                                          participation_ratio=pending.participation_ratio,
+                                          device_diag=pending.diag_dev)
             snapshots += 1
             emit(sinks.observable_rows, rho.time_tag, rows)
             emit(sinks.density_snapshot, rho, target)

@@ -244,11 +244,35 @@ def telegraph_fixture():
     np.savez_compressed(os.path.join(HERE, "telegraph.npz"), meta=json.dumps(meta), **arrays)
 
 
+def density_fixture():
+    """Reference dense <rho>: accumulate_density on a random stack and the
+    packed snapshots of a small run() (density.py:57-98)."""
+    from ctqw.density import accumulate_density
+
+    rng = np.random.default_rng(2024)
+    stack = rng.normal(size=(7, 30)) + 1j * rng.normal(size=(7, 30))
+    stack /= np.linalg.norm(stack, axis=1, keepdims=True)
+    rho = accumulate_density(stack, time_tag=0.25)
+    arrays = {"stack": stack, "packed": rho.packed}
+    space = JointSpace(lattice=build_lattice([8]), m=2)
+    cfg = RunConfig(space=space, model=CouplingModel(onsite_energy=0.1, tunneling=1.0, interaction=0.5),
+                    noise=NoiseSpec(target="both", levels=(-0.1, 0.1), rate=0.5),
+                    stepper=StepperConfig(backend="taylor", dt=0.05), realizations=5, steps=12, post_rate=4,
+                    master_seed=1234, workers=1, precision="double")
+    sinks = MemorySinks()
+    run(cfg, sinks)
+    meta = {"n": 8, "m": 2, "R": 5, "steps": 12, "post_rate": 4, "dt": 0.05, "rate": 0.5,
+            "snapshots": [(d.time_tag, d.sample_count) for d in sinks.densities]}
+    for i, d in enumerate(sinks.densities):
+        arrays[f"snap{i}"] = d.packed
+    np.savez_compressed(os.path.join(HERE, "density.npz"), meta=json.dumps(meta), **arrays)
+
+
 if __name__ == "__main__":
     import sys as _sys
 
     only = _sys.argv[1:]
-    for fn in (noise_fixture, stencil_fixture, segment_fixture, run_fixture, telegraph_fixture):
+    for fn in (noise_fixture, stencil_fixture, segment_fixture, run_fixture, telegraph_fixture, density_fixture):
         if not only or fn.__name__ in only:
             fn()
     for f in sorted(os.listdir(HERE)):

@@ -619,3 +619,37 @@ def test_init_process_advance_api_matches_reference(pkg):
         np.testing.assert_array_equal(np.stack([pr.values for pr in procs]), data[f"traj0_values_{k}"])
         np.testing.assert_array_equal([pr.switch_count for pr in procs], data[f"traj0_switches_{k}"])
     assert switched == int(data[f"traj0_switches_{c['checkpoints'][-1]}"].sum())
+
+
+# ---------------------------------------------------------------------------
+# dense <rho> (density.py:57-98)
+
+
+def test_accumulate_density_matches_reference(pkg):
+    p = pkg
+    data, _ = load_golden("density.npz")
+    rho = p.accumulate_density(data["stack"], time_tag=0.25)
+    assert rho.dim == 30 and rho.sample_count == 7 and rho.time_tag == 0.25
+    np.testing.assert_allclose(rho.packed, data["packed"], rtol=0, atol=1e-15)
+    assert rho.trace() == pytest.approx(1.0, abs=1e-14)
+    dense = rho.dense()
+    np.testing.assert_allclose(dense, dense.conj().T)
+
+
+def test_run_dense_snapshots_match_reference(pkg):
+    """run() with MemorySinks(dense=True): the packed <rho> snapshots of the
+    reference's run (dynamic noise, 3 collection points)."""
+    p = pkg
+    data, meta = load_golden("density.npz")
+    cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([meta["n"]]), meta["m"]),
+                      model=p.CouplingModel(onsite_energy=0.1, tunneling=1.0, interaction=0.5),
+                      noise=p.NoiseSpec(target="both", levels=(-0.1, 0.1), rate=meta["rate"]),
+                      stepper=p.StepperConfig(backend="taylor", dt=meta["dt"]), realizations=meta["R"],
+                      steps=meta["steps"], post_rate=meta["post_rate"], master_seed=1234, precision="double")
+    sinks = p.MemorySinks(dense=True)
+    p.run(cfg, sinks)
+    assert [(d.time_tag, d.sample_count) for d in sinks.densities] == [tuple(x) for x in meta["snapshots"]]
+    for i, d in enumerate(sinks.densities):
+        np.testing.assert_allclose(d.packed, data[f"snap{i}"], rtol=0, atol=1e-13)
+        assert d.purity == pytest.approx(float(2 * np.sum(np.abs(data[f"snap{i}"]) ** 2)
+                                               - np.sum(np.abs(np.diagonal(d.dense())) ** 2)), rel=1e-12)
