@@ -45,13 +45,16 @@ extern "C" {
 typedef struct ctqw_ctx *ctqw_handle_t;
 
 /* Geometry + deterministic couplings.  Replaces JointSpace/LatticeTopology
- * (hilbert.py:45-138) and CouplingModel (hamiltonian.py:30-72) for the
- * supported family: q = 1, periodic, k_half = 1, 1 <= m <= 3, n_sites >= 3. */
+ * (hilbert.py:45-138) and CouplingModel (hamiltonian.py:30-72), 1 <= m <= 3.
+ * The ring (k_half = 1, periodic = 1, n_sites >= 3) is complete as created
+ * and runs the fused kernels.  Any other lattice (q >= 1 directions, K =
+ * sum(k_half) slots per site, periodic or open) passes its move tables with
+ * ctqw_set_lattice and runs the generic kernels. */
 typedef struct {
   int32_t m;            /* particles */
-  int32_t n_sites;      /* ring length N */
-  int32_t k_half;       /* must be 1 */
-  int32_t periodic;     /* must be 1 */
+  int32_t n_sites;      /* lattice sites N = prod(dims) */
+  int32_t k_half;       /* K: positive move slots per site (1 for the ring) */
+  int32_t periodic;     /* 1 periodic, 0 open */
   double onsite_energy; /* eps0 */
   double tunneling;     /* t */
   double interaction;   /* U, per coinciding pair */
@@ -138,6 +141,14 @@ int ctqw_telegraph_advance(ctqw_handle_t h, int64_t count, double dt, void *stre
 int ctqw_telegraph_enable(ctqw_handle_t h, int32_t enable);
 int ctqw_telegraph_read(ctqw_handle_t h, double *values_dev, double *next_switch_dev, double *times_host,
                         int64_t *switches_host, void *stream);
+
+/* Move tables of a general lattice in the reference's slot order
+ * (_site_move_tables, hilbert.py:189-224): pos/neg[x*K + s] = target site of
+ * the +/- move of slot s from site x, -1 off an open lattice; t_slot[s] =
+ * tunnelling of slot s's direction (slot_couplings, hamiltonian.py:92-97).
+ * Links are x*K + s (hilbert.py:311), so hop rows hold N*K couplings. */
+int ctqw_set_lattice(ctqw_handle_t h, int32_t n_slots, const int32_t *pos_host, const int32_t *neg_host,
+                     const double *t_slot_host);
 
 int ctqw_build_coefficients(ctqw_handle_t h, const double *noise_dev, int64_t count,
                             int64_t n_links, int64_t n_sites, double *hop_dev,

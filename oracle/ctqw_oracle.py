@@ -49,8 +49,11 @@ class Stencil:
     m: int
     n: int
     base: np.ndarray          # (4,) diagonal base per coincidence count c
-    hop: np.ndarray           # (B, N) hop amplitude of link x -> x+1
+    hop: np.ndarray           # (B, N) hop amplitude of link x -> x+1 (ring); (B, N*K) link x*K+s (lattice)
     site: np.ndarray | None   # (B, N) on-site noise, None when absent
+    pos: np.ndarray | None = None    # (N, K) +move targets, -1 off-lattice (general lattices)
+    neg: np.ndarray | None = None    # (N, K) -move targets
+    t_slot: np.ndarray | None = None  # (K,) tunnelling per slot
 
     @property
     def dim(self) -> int:
@@ -75,6 +78,81 @@ def make_stencil(m, n, onsite, tunneling, interaction, link=None, site=None, bat
     else:
         site = None
     return Stencil(m=m, n=n, base=base, hop=hop, site=site)
+
+
+def make_lattice_stencil(m, dims, k_half, boundary, onsite, tunneling, interaction, link=None, site=None,
+                         batch=1):
+    """General lattice (hilbert.py:189-224, hamiltonian.py:92-141): the
+    single-particle move tables in the reference's slot order and the link
+    couplings ``t_dir(slot) + xi_link[x*K + s]``."""
+    dims = [int(d) for d in dims]
+    k_half = [int(k) for k in k_half]
+    q = len(dims)
+    n = int(np.prod(dims))
+    coords = np.empty((n, q), dtype=np.int64)
+    rem = np.arange(n, dtype=np.int64)
+    for i in range(q - 1, -1, -1):
+        coords[:, i] = rem % dims[i]
+        rem //= dims[i]
+    strides = [int(np.prod(dims[i + 1:])) for i in range(q)]
+    slots = [(i, d) for i in range(q) for d in range(1, k_half[i] + 1)]
+    pos = np.empty((n, len(slots)), dtype=np.int64)
+    neg = np.empty((n, len(slots)), dtype=np.int64)
+    base_sites = np.arange(n, dtype=np.int64)
+    for sl, (i, d) in enumerate(slots):
+        c = coords[:, i]
+        if boundary == "periodic":
+            pos[:, sl] = base_sites + ((c + d) % dims[i] - c) * strides[i]
+            neg[:, sl] = base_sites + ((c - d) % dims[i] - c) * strides[i]
+        else:
+            pos[:, sl] = np.where(c + d < dims[i], base_sites + d * strides[i], -1)
+            neg[:, sl] = np.where(c - d >= 0, base_sites - d * strides[i], -1)
+    per_dir = (np.asarray(tunneling, dtype=np.float64) if np.ndim(tunneling)
+               else np.full(q, float(tunneling)))
+    t_slot = per_dir[[i for i, _ in slots]]
+    K = len(slots)
+    t_links = np.tile(t_slot, n)                    # link x*K + s
+    if link is not None and np.shape(link)[-1]:
+        hop = t_links + np.atleast_2d(np.asarray(link, dtype=np.float64))
+    else:
+        hop = np.broadcast_to(t_links, (batch, n * K)).copy()
+    if site is not None and np.shape(site)[-1]:
+        site = np.atleast_2d(np.asarray(site, dtype=np.float64))
+    else:
+        site = None
+    return Stencil(m=m, n=n, base=diagonal_base(m, onsite, interaction), hop=hop, site=site, pos=pos, neg=neg,
+                   t_slot=t_slot)
+
+
+def _apply_lattice(st: Stencil, psi: np.ndarray, v0: np.ndarray) -> np.ndarray:
+    """``apply_values`` on a general lattice, order: diagonal, then per
+    particle p and slot s the +move, then the -move whose coupling is stored
+    at its target row (hamiltonian.py:205-222); absent moves add an exact
+    zero."""
+    m, n, K = st.m, st.n, st.pos.shape[1]
+    b = psi.shape[0]
+    dim = psi.shape[1]
+    out = v0.reshape(v0.shape[0], -1) * psi
+    alpha = np.arange(dim, dtype=np.int64)
+    digits = np.empty((dim, m), dtype=np.int64)
+    rem = alpha.copy()
+    for p in range(m - 1, -1, -1):
+        digits[:, p] = rem % n
+        rem //= n
+    hop = st.hop if st.hop.shape[0] == b else np.broadcast_to(st.hop, (b, st.hop.shape[1]))
+    for p in range(m):
+        shift = n ** (m - 1 - p)
+        xs = digits[:, p]
+        for sl in range(K):
+            tgt = st.pos[xs, sl]
+            ok = tgt >= 0
+            beta = np.where(ok, alpha + (tgt - xs) * shift, 0)
+            out = out + np.where(ok, hop[:, xs * K + sl] * psi[:, beta], 0)
+            src = st.neg[xs, sl]
+            ok = src >= 0
+            beta = np.where(ok, alpha + (src - xs) * shift, 0)
+            out = out + np.where(ok, hop[:, np.where(ok, src, 0) * K + sl] * psi[:, beta], 0)
+    return out
 
 
 def diagonal_values(st: Stencil) -> np.ndarray:
@@ -104,6 +182,8 @@ def diagonal_values(st: Stencil) -> np.ndarray:
 
 def apply_stencil(st: Stencil, psi: np.ndarray, v0: np.ndarray | None = None) -> np.ndarray:
     """``H psi`` for a (B, D) complex128 stack, reference accumulation order."""
+    if st.pos is not None:
+        return _apply_lattice(st, psi, diagonal_values(st) if v0 is None else v0)
     m, n = st.m, st.n
     b = psi.shape[0]
     shp = (b,) + (n,) * m
@@ -229,7 +309,8 @@ def refresh_stencil(st, noise, tunneling):
     (hamiltonian.py:131-141), which the reference's incremental ``update``
     reproduces bit for bit (test_hamiltonian.py:124-139)."""
     if noise.n_links:
-        st.hop = np.float64(tunneling) + noise.link_values()
+        t = np.tile(st.t_slot, st.n) if st.t_slot is not None else np.float64(tunneling)
+        st.hop = t + noise.link_values()
     if noise.n_sites:
         st.site = noise.site_values().copy()
 
@@ -282,14 +363,15 @@ def populations(jd: np.ndarray, m: int, n: int) -> np.ndarray:
     return out
 
 
-def position_stats(pops: np.ndarray, window=2, mass=1e-3):
-    """``observables.position_variance`` (observables.py:59-83), periodic ring."""
+def position_stats(pops: np.ndarray, window=2, mass=1e-3, periodic=True):
+    """``observables.position_variance`` (observables.py:59-83); the wrap flag
+    only on a periodic lattice."""
     marginal = pops / pops.sum()
     x = np.arange(marginal.shape[0], dtype=np.float64)
     mean = float(marginal @ x)
     var = float(marginal @ (x - mean) ** 2)
     wrapped = False
-    if marginal.shape[0] > 2 * window:
+    if periodic and marginal.shape[0] > 2 * window:
         wrapped = bool(marginal[:window].sum() > mass and marginal[-window:].sum() > mass)
     return mean, var, wrapped
 
@@ -305,7 +387,7 @@ def purity(stack: np.ndarray) -> float:
     return float((np.abs(g) ** 2).sum() / stack.shape[0] ** 2)
 
 
-def observable_rows(stack, m, n, observables):
+def observable_rows(stack, m, n, observables, periodic=True):
     """Row list in ``_observable_rows`` order (ensemble.py:609-632)."""
     jd = joint_distribution(stack)
     rows = []
@@ -313,7 +395,7 @@ def observable_rows(stack, m, n, observables):
         if name == "populations":
             rows.extend(("population", i, float(v)) for i, v in enumerate(populations(jd, m, n)))
         elif name == "position_mean_variance":
-            mean, var, wrapped = position_stats(populations(jd, m, n))
+            mean, var, wrapped = position_stats(populations(jd, m, n), periodic=periodic)
             rows += [("position_mean", 0, mean), ("position_variance", 0, var),
                      ("position_wrapped", 0, float(wrapped))]
         elif name == "purity":
@@ -350,7 +432,7 @@ def schedule(steps: int, post_rate: int):
 
 def run_rows(st, psi0, realizations, steps, post_rate, dt, hbar=1.0, backend="taylor", order=4,
              observables=("populations", "position_mean_variance", "purity", "participation_ratio"),
-             tol_norm=1e-6, tol_fail=1e-3, renormalize=True, noise=None, tunneling=1.0):
+             tol_norm=1e-6, tol_fail=1e-3, renormalize=True, noise=None, tunneling=1.0, periodic=True):
     """Diagonal-observable restatement of ``run`` (ensemble.py:635-804)."""
     psi = np.tile(psi0, (realizations, 1))
     out = []
@@ -366,5 +448,5 @@ def run_rows(st, psi0, realizations, steps, post_rate, dt, hbar=1.0, backend="ta
             totals.max_deviation = max(totals.max_deviation, stats.max_deviation)
             totals.events.extend(stats.events)
         prev = target
-        out.append((target * dt, observable_rows(psi, st.m, st.n, observables)))
+        out.append((target * dt, observable_rows(psi, st.m, st.n, observables, periodic)))
     return out, psi, totals

@@ -30,6 +30,15 @@ struct ctqw_ctx {
   const double* hop = nullptr;
   const double* site = nullptr;
   int64_t stride = 0;
+  int64_t site_stride = 0;
+  // lattice: K stored slots per site; general lattices carry move tables and
+  // run on the generic kernels only
+  int K = 1;
+  bool needs_lattice = false;  // created with k_half != 1 or open boundary
+  bool general = false;        // ctqw_set_lattice called
+  int* lat_pos = nullptr;
+  int* lat_neg = nullptr;
+  double* t_slot = nullptr;    // [K] tunnelling per slot (device)
   // library-owned device buffers
   double* levels = nullptr;
   int64_t levels_cap = 0;
@@ -200,9 +209,18 @@ StepScalars scalars_for(const ctqw_ctx* h, const ctqw_stepper_t* st) {
   return sc;
 }
 
-Coef coef_of(const ctqw_ctx* h) { return Coef{h->hop, h->site, h->stride}; }
+Coef coef_of(const ctqw_ctx* h) {
+  Coef c{h->hop, h->site, h->stride, h->site_stride};
+  if (h->general) {
+    c.pos = h->lat_pos;
+    c.neg = h->lat_neg;
+    c.K = h->K;
+  }
+  return c;
+}
 
 int check_bound(ctqw_ctx* h, int64_t count) {
+  if (h->needs_lattice && !h->general) return fail_with(h, CTQW_ERR_CONFIG, "no lattice tables (ctqw_set_lattice)");
   if (!h->hop) return fail_with(h, CTQW_ERR_CONFIG, "no coefficients bound (ctqw_bind_coefficients)");
   if (count < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative realization count");
   if (h->stride != 0 && count > h->coef_count)
@@ -267,9 +285,9 @@ int telegraph_step(ctqw_ctx* h, int64_t count, double dt, cudaStream_t s) {
   if (!h->tg_enabled) return CTQW_OK;
   if (count > h->tg_count) return fail_with(h, CTQW_ERR_CONFIG, "more realizations than the noise process holds");
   CUDA_TRY(h, launch_telegraph_advance(count, h->tg_total, h->tg_links, h->tg_sites, h->n, dt, h->tg_levels,
-                                       h->tg_nlev, h->tg_mean_wait, h->model.tunneling, h->tg_values, h->tg_next,
+                                       h->tg_nlev, h->tg_mean_wait, h->t_slot, h->K, h->tg_values, h->tg_next,
                                        h->tg_gen, const_cast<double*>(h->hop), const_cast<double*>(h->site),
-                                       h->stride, h->fail, s));
+                                       h->stride, h->site_stride, h->fail, s));
   h->launches += 1;
   return CTQW_OK;
 }
@@ -288,11 +306,11 @@ int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
   const ctqw_model_t& md = *model;
   if (md.m < 1 || md.m > 3)
     return fail_with(nullptr, CTQW_ERR_CONFIG, "the B200 path supports 1 <= m <= 3 particles");
-  if (md.n_sites < 3)
+  if (md.n_sites < 2) return fail_with(nullptr, CTQW_ERR_CONFIG, "the lattice needs n_sites >= 2");
+  if (md.k_half < 1) return fail_with(nullptr, CTQW_ERR_CONFIG, "k_half (slots per site) must be >= 1");
+  const bool ring = md.k_half == 1 && md.periodic == 1;
+  if (ring && md.n_sites < 3)
     return fail_with(nullptr, CTQW_ERR_CONFIG, "ring needs n_sites >= 3 (2*k_half < extent)");
-  if (md.k_half != 1 || md.periodic != 1)
-    return fail_with(nullptr, CTQW_ERR_CONFIG,
-                     "the B200 path supports periodic nearest-neighbour rings (k_half = 1)");
   for (double v : {md.onsite_energy, md.tunneling, md.interaction, md.hbar})
     if (!std::isfinite(v)) return fail_with(nullptr, CTQW_ERR_CONFIG, "model parameters must be finite");
   if (!(md.hbar > 0)) return fail_with(nullptr, CTQW_ERR_CONFIG, "hbar must be > 0");
@@ -310,6 +328,8 @@ int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
   h->model = md;
   h->m = md.m;
   h->n = md.n_sites;
+  h->K = md.k_half;
+  h->needs_lattice = !ring;
   h->dim = 1;
   for (int p = 0; p < md.m; ++p) h->dim *= md.n_sites;
   for (int c = 0; c < 4; ++c) {
@@ -328,6 +348,13 @@ int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
   }
   long long nf = kNoFail;
   cudaMemcpy(h->fail, &nf, sizeof(nf), cudaMemcpyHostToDevice);
+  // ring slot coupling (one slot, the model's t); ctqw_set_lattice replaces it
+  if (cudaMalloc((void**)&h->t_slot, sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    ctqw_destroy(h);
+    return fail_with(nullptr, CTQW_ERR_OTHER, "cannot allocate handle buffers");
+  }
+  cudaMemcpy(h->t_slot, &md.tunneling, sizeof(double), cudaMemcpyHostToDevice);
   if (const char* sk = std::getenv("CTQW_STREAM")) {
     h->stream_kind = std::strcmp(sk, "tile") == 0    ? 1
                      : std::strcmp(sk, "band") == 0  ? 2
@@ -347,7 +374,8 @@ int ctqw_destroy(ctqw_handle_t h) {
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   void* dev_ptrs[] = {h->levels, h->partial, h->scl, h->stats, h->events, h->fail,
                       h->summary_dev, h->scratch[0], h->scratch[1], h->n2_dev, h->small,
-                      h->overlap_partial, h->tg_values, h->tg_next, h->tg_gen, h->tg_levels, h->tg_sum};
+                      h->overlap_partial, h->tg_values, h->tg_next, h->tg_gen, h->tg_levels, h->tg_sum,
+                      h->lat_pos, h->lat_neg, h->t_slot};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (h->summary_host) cudaFreeHost(h->summary_host);
@@ -382,8 +410,8 @@ int ctqw_telegraph_init(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64
   if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
   if (n_levels < 1 || !levels_host) return fail_with(h, CTQW_ERR_CONFIG, "noise level set is empty");
   if (r0 < 0 || count < 0 || n_links < 0 || n_sites < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative sizes");
-  if ((n_links != 0 && n_links != h->n) || (n_sites != 0 && n_sites != h->n))
-    return fail_with(h, CTQW_ERR_CONFIG, "noise rows must hold 0 or N links and 0 or N sites");
+  if ((n_links != 0 && n_links != (int64_t)h->n * h->K) || (n_sites != 0 && n_sites != h->n))
+    return fail_with(h, CTQW_ERR_CONFIG, "noise rows must hold 0 or N*K links and 0 or N sites");
   if (!(rate > 0.0) || !std::isfinite(rate)) return fail_with(h, CTQW_ERR_CONFIG, "telegraph rate must be > 0");
   for (int i = 0; i < n_levels; ++i)
     if (!std::isfinite(levels_host[i])) return fail_with(h, CTQW_ERR_CONFIG, "noise levels must be finite");
@@ -430,10 +458,10 @@ int ctqw_telegraph_advance(ctqw_handle_t h, int64_t count, double dt, void* stre
   DeviceGuard g(h->device);
   const bool coef = h->hop && h->coef_count >= count;
   CUDA_TRY(h, launch_telegraph_advance(count, h->tg_total, h->tg_links, h->tg_sites, h->n, dt, h->tg_levels,
-                                       h->tg_nlev, h->tg_mean_wait, h->model.tunneling, h->tg_values, h->tg_next,
+                                       h->tg_nlev, h->tg_mean_wait, h->t_slot, h->K, h->tg_values, h->tg_next,
                                        h->tg_gen, coef ? const_cast<double*>(h->hop) : nullptr,
-                                       coef ? const_cast<double*>(h->site) : nullptr, h->stride, nullptr,
-                                       (cudaStream_t)stream));
+                                       coef ? const_cast<double*>(h->site) : nullptr, h->stride, h->site_stride,
+                                       nullptr, (cudaStream_t)stream));
   h->launches += 1;
   return CTQW_OK;
 }
@@ -467,16 +495,46 @@ int ctqw_telegraph_read(ctqw_handle_t h, double* values_dev, double* next_switch
   return CTQW_OK;
 }
 
+int ctqw_set_lattice(ctqw_handle_t h, int32_t n_slots, const int32_t* pos_host, const int32_t* neg_host,
+                     const double* t_slot_host) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (n_slots != h->K) return fail_with(h, CTQW_ERR_CONFIG, "n_slots must equal the model's k_half (slots per site)");
+  if (!pos_host || !neg_host || !t_slot_host) return fail_with(h, CTQW_ERR_CONFIG, "NULL lattice table");
+  const int64_t nk = (int64_t)h->n * n_slots;
+  for (int64_t i = 0; i < nk; ++i)
+    if (pos_host[i] < -1 || pos_host[i] >= h->n || neg_host[i] < -1 || neg_host[i] >= h->n)
+      return fail_with(h, CTQW_ERR_CONFIG, "lattice move targets out of range");
+  for (int s = 0; s < n_slots; ++s)
+    if (!std::isfinite(t_slot_host[s])) return fail_with(h, CTQW_ERR_CONFIG, "tunneling amplitudes must be finite");
+  DeviceGuard g(h->device);
+  for (int** p : {&h->lat_pos, &h->lat_neg}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (cudaMalloc((void**)p, nk * sizeof(int)) != cudaSuccess)
+      return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate lattice tables");
+  }
+  if (h->t_slot) cudaFree(h->t_slot);
+  h->t_slot = nullptr;
+  if (cudaMalloc((void**)&h->t_slot, n_slots * sizeof(double)) != cudaSuccess)
+    return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate lattice tables");
+  CUDA_TRY(h, cudaMemcpy(h->lat_pos, pos_host, nk * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(h->lat_neg, neg_host, nk * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(h->t_slot, t_slot_host, n_slots * sizeof(double), cudaMemcpyHostToDevice));
+  h->general = true;
+  return CTQW_OK;
+}
+
 int ctqw_build_coefficients(ctqw_handle_t h, const double* noise_dev, int64_t count,
                             int64_t n_links, int64_t n_sites, double* hop_dev, double* site_dev,
                             void* stream) {
   if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
-  if ((n_links != 0 && n_links != h->n) || (n_sites != 0 && n_sites != h->n))
-    return fail_with(h, CTQW_ERR_CONFIG, "noise rows must hold 0 or N links and 0 or N sites");
+  if ((n_links != 0 && n_links != (int64_t)h->n * h->K) || (n_sites != 0 && n_sites != h->n))
+    return fail_with(h, CTQW_ERR_CONFIG, "noise rows must hold 0 or N*K links and 0 or N sites");
   if (n_sites && !site_dev) return fail_with(h, CTQW_ERR_CONFIG, "site_dev required for on-site noise");
   if ((n_links || n_sites) && !noise_dev) return fail_with(h, CTQW_ERR_CONFIG, "noise_dev is NULL");
+  if (h->needs_lattice && !h->general) return fail_with(h, CTQW_ERR_CONFIG, "no lattice tables (ctqw_set_lattice)");
   DeviceGuard g(h->device);
-  CUDA_TRY(h, launch_build_coef(noise_dev, count, h->n, n_links, n_sites, h->model.tunneling,
+  CUDA_TRY(h, launch_build_coef(noise_dev, count, h->n, h->K, n_links, n_sites, h->t_slot,
                                 hop_dev, site_dev, (cudaStream_t)stream));
   h->launches += 1;
   return CTQW_OK;
@@ -486,11 +544,12 @@ int ctqw_bind_coefficients(ctqw_handle_t h, int64_t count, const double* hop_dev
                            const double* site_dev, int64_t stride) {
   if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
   if (!hop_dev) return fail_with(h, CTQW_ERR_CONFIG, "hop_dev is NULL");
-  if (stride != 0 && stride != h->n) return fail_with(h, CTQW_ERR_CONFIG, "stride must be 0 or N");
+  if (stride != 0 && stride != (int64_t)h->n * h->K) return fail_with(h, CTQW_ERR_CONFIG, "stride must be 0 or N*K");
   h->coef_count = count;
   h->hop = hop_dev;
   h->site = site_dev;
   h->stride = stride;
+  h->site_stride = stride ? h->n : 0;
   return CTQW_OK;
 }
 
@@ -625,8 +684,10 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   double2* psi = (double2*)psi_dev;
   double2* work = (double2*)work_dev;
 
-  // a pinned streaming family (CTQW_STREAM) bypasses the resident path
-  if (h->stream_kind == 0 && resident_supported(h->m, h->n, sc)) {
+  if (h->needs_lattice && !h->general) return fail_with(h, CTQW_ERR_CONFIG, "no lattice tables (ctqw_set_lattice)");
+  // a pinned streaming family (CTQW_STREAM) bypasses the resident path;
+  // general lattices (move tables) run on the generic kernels only
+  if (h->stream_kind == 0 && !h->general && resident_supported(h->m, h->n, sc)) {
     h->stream_kernel = "resident_kernel";
     // dynamic noise changes the couplings after every step: one step per launch
     const int64_t chunk = h->tg_enabled ? 1 : n_steps;
@@ -648,7 +709,7 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   // CTQW_STREAM pins one kernel family (A/B measurements, per-kernel parity
   // tests); a pinned family that does not support the case falls through
   // to the next one in auto order.
-  const int kind = h->stream_kind;
+  const int kind = h->general ? 6 : h->stream_kind;
   const bool use_band4 = (kind == 0 || kind == 4) && band4_supported(h->m, h->n, sc);
   const bool use_plane3 = (kind == 0 || kind == 5) && plane3_supported(h->m, h->n, sc);
   const bool use_band2 = !use_band4 && (kind == 0 || kind == 3 || kind == 4) &&

@@ -17,11 +17,20 @@ namespace ctqw {
 constexpr int kMaxEvents = 100;     // ensemble.py:119
 constexpr long long kNoFail = 0x7fffffffffffffffLL;
 
-// Coefficient rows of a batch: realization i reads hop + i*stride.
+// Coefficient rows of a batch: realization i reads hop + i*stride and
+// site + i*site_stride.  Ring (q = 1, K = 1, periodic): hop[x] couples
+// x -> x+1.  General lattices (pos != nullptr, generic kernels only):
+// hop[x*K + s] couples x -> pos[x*K + s] (the reference's link
+// x*K + s, hilbert.py:303-314), pos / neg = targets of the signed moves,
+// -1 off-lattice (hilbert.py:189-224).
 struct Coef {
-  const double* hop;    // [.][N]  t + xi_link[x] for the link x -> x+1
-  const double* site;   // [.][N]  xi_site[x], nullptr when absent
+  const double* hop;    // [.][N*K]  t_dir + xi_link
+  const double* site;   // [.][N]    xi_site[x], nullptr when absent
   int64_t stride;       // 0 = broadcast
+  int64_t site_stride;
+  const int* pos = nullptr;  // [N][K] general lattice move tables (device)
+  const int* neg = nullptr;
+  int K = 1;
 };
 
 // Norm policy, StepperConfig (propagators.py:61-86).

@@ -30,8 +30,8 @@ int generic_parts(int64_t dim);
 cudaError_t launch_draw_noise(uint64_t master_seed, int64_t r0, int64_t count,
                               const double* levels_dev, int n_levels, int64_t total,
                               double* out, cudaStream_t s);
-cudaError_t launch_build_coef(const double* noise, int64_t count, int n, int64_t n_links,
-                              int64_t n_sites, double t, double* hop, double* site,
+cudaError_t launch_build_coef(const double* noise, int64_t count, int n, int K, int64_t n_links,
+                              int64_t n_sites, const double* t_slot, double* hop, double* site,
                               cudaStream_t s);
 cudaError_t launch_fill_states(double2* psi, int64_t count, int64_t dim, const double2* psi0,
                                cudaStream_t s);
@@ -50,9 +50,9 @@ cudaError_t launch_telegraph_init(uint64_t master_seed, int64_t r0, int64_t coun
 size_t telegraph_advance_smem(int64_t total);
 cudaError_t launch_telegraph_advance(int64_t count, int64_t total, int64_t n_links, int64_t n_sites, int n,
                                      double dt, const double* levels_dev, int n_levels, double mean_wait,
-                                     double t_hop, double* values, double* next_switch, TelegraphGen* gen,
-                                     double* hop, double* site, int64_t coef_stride, const long long* fail,
-                                     cudaStream_t s);
+                                     const double* t_slot, int K, double* values, double* next_switch,
+                                     TelegraphGen* gen, double* hop, double* site, int64_t hop_stride,
+                                     int64_t site_stride, const long long* fail, cudaStream_t s);
 
 // stencil_generic.cu
 cudaError_t launch_apply(int m, const double2* psi, double2* out, int64_t count, int64_t dim,

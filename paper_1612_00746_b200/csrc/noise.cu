@@ -32,18 +32,21 @@ __global__ void draw_noise_kernel(uint64_t master_seed, int64_t r0, int64_t coun
   for (int64_t k = 0; k < total; ++k) row[k] = levels[b.draw(g, c)];
 }
 
-// hop = t + xi_link (hamiltonian.py:137-141: out[...,1:] = base; += link),
-// site = xi_site.  Without link noise hop = t exactly.
-__global__ void build_coef_kernel(const double* __restrict__ noise, int64_t count, int n,
-                                  int64_t n_links, int64_t n_sites, double t,
+// hop = t_dir + xi_link (hamiltonian.py:137-141: out[...,1:] = base; += link),
+// site = xi_site.  Links are laid out x*K + s (hilbert.py:311); slot s has
+// the tunnelling t_slot[s] of its direction.  Without link noise hop = t.
+__global__ void build_coef_kernel(const double* __restrict__ noise, int64_t count, int n, int K,
+                                  int64_t n_links, int64_t n_sites, const double* __restrict__ t_slot,
                                   double* __restrict__ hop, double* __restrict__ site) {
   const int64_t total = n_links + n_sites;
+  const int64_t nk = (int64_t)n * K;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count * n) return;
-  const int64_t r = i / n, x = i % n;
+  if (i >= count * nk) return;
+  const int64_t r = i / nk, l = i % nk;
   const double* row = noise + r * total;
-  hop[i] = n_links ? __dadd_rn(t, row[x]) : t;
-  if (n_sites && site) site[i] = row[n_links + x];
+  const double t = t_slot[l % K];
+  hop[i] = n_links ? __dadd_rn(t, row[l]) : t;
+  if (n_sites && site && l < n) site[r * n + l] = row[n_links + l];
 }
 
 __global__ void fill_states_kernel(double2* __restrict__ psi, int64_t count, int64_t dim,
@@ -65,14 +68,14 @@ cudaError_t launch_draw_noise(uint64_t master_seed, int64_t r0, int64_t count,
   return cudaGetLastError();
 }
 
-cudaError_t launch_build_coef(const double* noise, int64_t count, int n, int64_t n_links,
-                              int64_t n_sites, double t, double* hop, double* site,
+cudaError_t launch_build_coef(const double* noise, int64_t count, int n, int K, int64_t n_links,
+                              int64_t n_sites, const double* t_slot, double* hop, double* site,
                               cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  const int64_t work = count * n;
+  const int64_t work = count * n * K;
   const int bs = 256;
-  build_coef_kernel<<<(unsigned)((work + bs - 1) / bs), bs, 0, s>>>(noise, count, n, n_links,
-                                                                     n_sites, t, hop, site);
+  build_coef_kernel<<<(unsigned)((work + bs - 1) / bs), bs, 0, s>>>(noise, count, n, K, n_links, n_sites, t_slot,
+                                                                     hop, site);
   return cudaGetLastError();
 }
 

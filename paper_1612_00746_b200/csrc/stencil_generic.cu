@@ -81,6 +81,70 @@ __device__ __forceinline__ double2 stencil_point(const double2* __restrict__ t, 
   return acc;
 }
 
+// General lattices (q >= 1, K = sum(k_half) slots per site, periodic or
+// open): the same accumulation order -- diagonal, then for each particle p
+// and site slot s the +move and the -move (stored slot j = 1 + p*K + s,
+// hamiltonian.py:205-222).  The -move reads the coupling stored at its
+// target row: the link of the target site, hop[neg*K + s].  Moves off an
+// open lattice contribute nothing (the reference adds an exact zero).
+template <int M, bool EXACT, bool SITE, bool SCALE>
+__device__ __forceinline__ double2 stencil_point_lat(const double2* __restrict__ t, int64_t a, int n,
+                                                     const double* __restrict__ hop,
+                                                     const double* __restrict__ site, const Coef& coef,
+                                                     const StencilConst& k, double s) {
+  const Digits<M> d = digits_of<M>(a, n);
+  int c = 0;
+#pragma unroll
+  for (int p = 0; p < M; ++p)
+#pragma unroll
+    for (int q = p + 1; q < M; ++q) c += (d.x[p] == d.x[q]);
+  double v0 = k.base[c];
+  if (SITE) {
+    double ss = site[d.x[0]];
+#pragma unroll
+    for (int p = 1; p < M; ++p) ss = __dadd_rn(ss, site[d.x[p]]);
+    v0 = __dadd_rn(v0, ss);
+  }
+  double2 self = t[a];
+  if (SCALE) self = rmul(s, self);
+  double2 acc = rmul(v0, self);
+  int64_t stride = 1;
+  int64_t strides[M];
+#pragma unroll
+  for (int p = M - 1; p >= 0; --p) {
+    strides[p] = stride;
+    stride *= n;
+  }
+  const int K = coef.K;
+#pragma unroll
+  for (int p = 0; p < M; ++p) {
+    const int xp = d.x[p];
+    for (int sl = 0; sl < K; ++sl) {
+      const int tgt = coef.pos[xp * K + sl];
+      if (tgt >= 0) {
+        double2 z = t[a + (int64_t)(tgt - xp) * strides[p]];
+        if (SCALE) z = rmul(s, z);
+        acc = madd<EXACT>(acc, hop[xp * K + sl], z);
+      }
+      const int src = coef.neg[xp * K + sl];
+      if (src >= 0) {
+        double2 z = t[a + (int64_t)(src - xp) * strides[p]];
+        if (SCALE) z = rmul(s, z);
+        acc = madd<EXACT>(acc, hop[src * K + sl], z);
+      }
+    }
+  }
+  return acc;
+}
+
+template <int M, bool EXACT, bool SITE, bool SCALE>
+__device__ __forceinline__ double2 stencil_any(const double2* __restrict__ t, int64_t a, int n,
+                                               const double* __restrict__ hop, const double* __restrict__ site,
+                                               const Coef& coef, const StencilConst& k, double s) {
+  if (coef.pos) return stencil_point_lat<M, EXACT, SITE, SCALE>(t, a, n, hop, site, coef, k, s);
+  return stencil_point<M, EXACT, SITE, SCALE>(t, a, n, hop, site, k, s);
+}
+
 template <int M, bool EXACT, bool SITE>
 __global__ void __launch_bounds__(kBlock) apply_kernel(const double2* __restrict__ psi,
                                                        double2* __restrict__ out, int64_t dim,
@@ -89,10 +153,10 @@ __global__ void __launch_bounds__(kBlock) apply_kernel(const double2* __restrict
   const int64_t r = r_base + blockIdx.y;
   const double2* t = psi + r * dim;
   const double* hop = coef.hop + r * coef.stride;
-  const double* site = SITE ? coef.site + r * coef.stride : nullptr;
+  const double* site = SITE ? coef.site + r * coef.site_stride : nullptr;
   for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < dim;
        a += (int64_t)gridDim.x * kBlock)
-    out[r * dim + a] = stencil_point<M, EXACT, SITE, false>(t, a, n, hop, site, k, 1.0);
+    out[r * dim + a] = stencil_any<M, EXACT, SITE, false>(t, a, n, hop, site, coef, k, 1.0);
 }
 
 // One Taylor order: term_out = (coeff/j) * H term_in; acc_out = acc_in + term_out
@@ -111,11 +175,11 @@ __global__ void __launch_bounds__(kBlock) taylor_order_kernel(
   const double s = SCALE ? scl[r] : 1.0;
   const double2* t = term_in + r * dim;
   const double* hop = coef.hop + r * coef.stride;
-  const double* site = SITE ? coef.site + r * coef.stride : nullptr;
+  const double* site = SITE ? coef.site + r * coef.site_stride : nullptr;
   double nrm = 0.0;
   for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < dim;
        a += (int64_t)gridDim.x * kBlock) {
-    const double2 h = stencil_point<M, EXACT, SITE, SCALE>(t, a, n, hop, site, k, s);
+    const double2 h = stencil_any<M, EXACT, SITE, SCALE>(t, a, n, hop, site, coef, k, s);
     const double2 tk = times_i(ci, h);
     double2 acc = acc_in[r * dim + a];
     if (SCALE) acc = rmul(s, acc);
@@ -147,7 +211,7 @@ __global__ void __launch_bounds__(kBlock) rk4_stage_kernel(
   const int64_t r = r_base + blockIdx.y;
   const double s = SCALE ? scl[r] : 1.0;
   const double* hop = coef.hop + r * coef.stride;
-  const double* site = SITE ? coef.site + r * coef.stride : nullptr;
+  const double* site = SITE ? coef.site + r * coef.site_stride : nullptr;
   const double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
   double nrm = 0.0;
   for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < dim;
@@ -156,9 +220,9 @@ __global__ void __launch_bounds__(kBlock) rk4_stage_kernel(
     // arg_in of stage 1 is psi itself (scaled); later stages read unscaled scratch
     double2 h;
     if (stage == 1)
-      h = stencil_point<M, EXACT, SITE, SCALE>(arg_in + r * dim, a, n, hop, site, k, s);
+      h = stencil_any<M, EXACT, SITE, SCALE>(arg_in + r * dim, a, n, hop, site, coef, k, s);
     else
-      h = stencil_point<M, EXACT, SITE, false>(arg_in + r * dim, a, n, hop, site, k, 1.0);
+      h = stencil_any<M, EXACT, SITE, false>(arg_in + r * dim, a, n, hop, site, coef, k, 1.0);
     const double2 st = times_i(ci, h);
     double2 p0 = make_double2(0.0, 0.0);
     if (stage < 4) {

@@ -66,9 +66,10 @@ constexpr int kAdvWarps = 4;
 // and the original due list whose old values decide "changed").
 __global__ void __launch_bounds__(32 * kAdvWarps) telegraph_advance_kernel(
     int64_t count, int64_t total, int64_t n_links, int64_t n_sites, int n, double dt,
-    const double* __restrict__ levels, int n_levels, double mean_wait, double t_hop,
+    const double* __restrict__ levels, int n_levels, double mean_wait, const double* __restrict__ t_slot, int K,
     double* __restrict__ values, double* __restrict__ next_switch, TelegraphGen* __restrict__ gen,
-    double* __restrict__ hop, double* __restrict__ site, int64_t coef_stride, const long long* fail) {
+    double* __restrict__ hop, double* __restrict__ site, int64_t hop_stride, int64_t site_stride,
+    const long long* fail) {
   extern __shared__ int adv_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * kAdvWarps + warp;
@@ -132,9 +133,9 @@ __global__ void __launch_bounds__(32 * kAdvWarps) telegraph_advance_kernel(
     const double nv = v[e];
     if (nv != oldv[q]) {
       if (e < n_links) {
-        if (hop) hop[r * coef_stride + e] = __dadd_rn(t_hop, nv);
+        if (hop) hop[r * hop_stride + e] = __dadd_rn(t_slot[e % K], nv);
       } else if (site) {
-        site[r * coef_stride + (e - n_links)] = nv;
+        site[r * site_stride + (e - n_links)] = nv;
       }
     }
   }
@@ -162,9 +163,9 @@ size_t telegraph_advance_smem(int64_t total) {
 
 cudaError_t launch_telegraph_advance(int64_t count, int64_t total, int64_t n_links, int64_t n_sites, int n,
                                      double dt, const double* levels_dev, int n_levels, double mean_wait,
-                                     double t_hop, double* values, double* next_switch, TelegraphGen* gen,
-                                     double* hop, double* site, int64_t coef_stride, const long long* fail,
-                                     cudaStream_t s) {
+                                     const double* t_slot, int K, double* values, double* next_switch,
+                                     TelegraphGen* gen, double* hop, double* site, int64_t hop_stride,
+                                     int64_t site_stride, const long long* fail, cudaStream_t s) {
   if (count <= 0 || total <= 0) return cudaSuccess;
   const size_t smem = telegraph_advance_smem(total);
   static size_t configured = 0;
@@ -175,8 +176,8 @@ cudaError_t launch_telegraph_advance(int64_t count, int64_t total, int64_t n_lin
     configured = smem;
   }
   telegraph_advance_kernel<<<(unsigned)((count + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps, smem, s>>>(
-      count, total, n_links, n_sites, n, dt, levels_dev, n_levels, mean_wait, t_hop, values, next_switch, gen,
-      hop, site, coef_stride, fail);
+      count, total, n_links, n_sites, n, dt, levels_dev, n_levels, mean_wait, t_slot, K, values, next_switch, gen,
+      hop, site, hop_stride, site_stride, fail);
   return cudaGetLastError();
 }
 

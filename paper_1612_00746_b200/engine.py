@@ -31,7 +31,7 @@ import numpy as np
 from . import sharding
 from .errors import CapacityError, ConfigurationError, MemoryBudgetError, NormFailureError
 from .geometry import JointSpace, build_topology, joint_index
-from .hamiltonian import CouplingModel, handle_for
+from .hamiltonian import CouplingModel, handle_for, model_handle
 from .noise import NoiseSpec, draw_noise
 from .observables import DiagonalDensity, position_stats_from_populations
 from .profiling import (
@@ -329,8 +329,7 @@ class EnsembleState:
         space = config.space
         self.topology = build_topology(space)
         model = config.model
-        self.handle = handle_for(space.m, space.lattice.n_sites, model.onsite_energy,
-                                 model.ring_tunneling(), model.interaction, model.hbar, device)
+        self.handle = model_handle(self.topology, model, device=device)
         self.dev = torch.device(f"cuda:{device}")
         n = space.lattice.n_sites
         self.dynamic = not config.noise.is_static
@@ -338,7 +337,7 @@ class EnsembleState:
             # telegraph process on the device (noise.py:128-206): values and
             # switch times drawn from the same NumPy-compatible streams, advanced
             # by ctqw_evolve after every step
-            n_links, n_sites = config.noise.element_counts(n)
+            n_links, n_sites = config.noise.element_counts(n, space.lattice.moves_half)
             if config.master_seed < 0 or lo < 0:
                 raise ConfigurationError("seeds must be non-negative")
             self.handle.telegraph_init(config.master_seed, lo, self.count, config.noise.levels, n_links,
@@ -346,9 +345,10 @@ class EnsembleState:
             noise = None
         else:
             noise, n_links, n_sites = draw_noise(self.handle, config.noise, config.master_seed, lo,
-                                                 self.count)
+                                                 self.count,
+                                                 config.noise.element_counts(n, space.lattice.moves_half))
         self.n_links, self.n_sites = n_links, n_sites
-        self.hop = torch.empty((max(self.count, 1), n), dtype=torch.float64, device=self.dev)
+        self.hop = torch.empty((max(self.count, 1), self.topology.n_links), dtype=torch.float64, device=self.dev)
         self.site = (torch.empty((max(self.count, 1), n), dtype=torch.float64, device=self.dev)
                      if n_sites else None)
         if self.count:
@@ -358,7 +358,7 @@ class EnsembleState:
             else:
                 self.handle.build_coefficients(noise.contiguous(), self.count, n_links, n_sites,
                                                self.hop, self.site)
-        self.handle.bind(self.hop, self.site, self.count, n)
+        self.handle.bind(self.hop, self.site, self.count, self.topology.n_links)
         self.handle.telegraph_enable(self.dynamic and self.count > 0)
         del noise
         psi0 = build_initial_state(config.initial, space)

@@ -4,12 +4,13 @@ Mirrors the reference's geometry API (``hilbert.py:45-173``): ``build_lattice``,
 ``LatticeTopology``, ``JointSpace``, ``joint_index``, ``joint_positions``.
 ``build_topology`` differs by design: the reference materialises an int64
 neighbour table of ``dim x (2H+1)`` entries (``hilbert.py:278-359``, 40 MiB at
-N = 1024); on the B200 path the kernels compute neighbours arithmetically, so
-the "topology" is just the ring stencil descriptor ``RingStencil``.
-
-Supported by the device path: one periodic direction, nearest-neighbour hops
-(q = 1, k_half = 1), 1 <= m <= 3.  Other lattices validate here but are
-rejected by ``build_topology`` (next round).
+N = 1024); on the B200 path the kernels compute joint neighbours on the fly,
+so the "topology" is the stencil descriptor ``LatticeStencil``: nothing for
+the periodic nearest-neighbour ring (the fused kernels), and for any other
+lattice -- q directions, k_half hops per direction, periodic or open -- the
+single-particle move tables of ``_site_move_tables`` (``hilbert.py:189-224``,
+N x K entries), which the generic kernels combine per particle.
+1 <= m <= 3 particles.
 """
 
 from __future__ import annotations
@@ -124,15 +125,63 @@ def joint_positions(alpha, space: JointSpace):
     return out
 
 
-@dataclass(frozen=True)
-class RingStencil:
-    """The B200 'topology': m particles on a periodic N-ring, K = 1.
+def site_coordinates(lattice: LatticeTopology, sites=None) -> np.ndarray:
+    """Row-major coordinates of each site (hilbert.py:176-186)."""
+    if sites is None:
+        sites = np.arange(lattice.n_sites, dtype=np.int64)
+    rem = np.asarray(sites, dtype=np.int64).copy()
+    coords = np.empty(rem.shape + (lattice.q,), dtype=np.int64)
+    for i in range(lattice.q - 1, -1, -1):
+        coords[..., i] = rem % lattice.dims[i]
+        rem //= lattice.dims[i]
+    return coords
 
-    Replaces the reference's materialised ``TopologyMatrix`` (hilbert.py:227-275);
-    ``half`` and ``dim`` keep their meaning.
+
+def site_move_tables(lattice: LatticeTopology):
+    """(pos, neg, directions, distances): targets of every signed
+    single-particle move, -1 off an open lattice; slots run direction-major,
+    distance 1..k_half within a direction (hilbert.py:189-224)."""
+    n, q = lattice.n_sites, lattice.q
+    coords = site_coordinates(lattice)
+    strides = np.empty(q, dtype=np.int64)
+    acc = 1
+    for i in range(q - 1, -1, -1):
+        strides[i] = acc
+        acc *= lattice.dims[i]
+    slots = [(i, dist) for i in range(q) for dist in range(1, lattice.k_half[i] + 1)]
+    pos = np.empty((n, len(slots)), dtype=np.int64)
+    neg = np.empty((n, len(slots)), dtype=np.int64)
+    base = np.arange(n, dtype=np.int64)
+    periodic = lattice.boundary == BOUNDARY_PERIODIC
+    for s, (i, dist) in enumerate(slots):
+        c = coords[:, i]
+        extent = lattice.dims[i]
+        if periodic:
+            pos[:, s] = base + ((c + dist) % extent - c) * strides[i]
+            neg[:, s] = base + ((c - dist) % extent - c) * strides[i]
+        else:
+            pos[:, s] = np.where(c + dist < extent, base + dist * strides[i], -1)
+            neg[:, s] = np.where(c - dist >= 0, base - dist * strides[i], -1)
+    directions = np.array([i for i, _ in slots], dtype=np.int64)
+    distances = np.array([d for _, d in slots], dtype=np.int64)
+    return pos, neg, directions, distances
+
+
+@dataclass(frozen=True)
+class LatticeStencil:
+    """The B200 'topology' of m particles on a lattice.
+
+    Replaces the reference's materialised ``TopologyMatrix``
+    (hilbert.py:227-275); ``half`` and ``dim`` keep their meaning.  The
+    periodic nearest-neighbour ring (``is_ring``) needs no tables; other
+    lattices carry the single-particle move tables.
     """
 
     space: JointSpace
+
+    @property
+    def lattice(self) -> LatticeTopology:
+        return self.space.lattice
 
     @property
     def m(self) -> int:
@@ -151,23 +200,37 @@ class RingStencil:
         return self.space.moves_half
 
     @property
+    def K(self) -> int:
+        return self.space.lattice.moves_half
+
+    @property
     def n_links(self) -> int:
-        return self.n * self.space.lattice.moves_half
+        return self.n * self.K
+
+    @property
+    def is_ring(self) -> bool:
+        lat = self.space.lattice
+        return lat.q == 1 and lat.k_half == (1,) and lat.boundary == BOUNDARY_PERIODIC
+
+    def move_tables(self):
+        """(pos, neg) int arrays (N, K) and the slot directions (K,)."""
+        pos, neg, directions, _ = site_move_tables(self.space.lattice)
+        return pos, neg, directions
+
+
+RingStencil = LatticeStencil
 
 
 def check_supported(space: JointSpace):
     lat = space.lattice
-    if lat.q != 1 or lat.k_half != (1,) or lat.boundary != BOUNDARY_PERIODIC:
-        raise ConfigurationError(
-            "the B200 path supports one periodic direction with nearest-neighbour hops "
-            f"(got dims={lat.dims}, k_half={lat.k_half}, boundary={lat.boundary!r})"
-        )
     if not 1 <= space.m <= 3:
         raise ConfigurationError(f"the B200 path supports 1 <= m <= 3 particles (got m={space.m})")
-    if lat.n_sites < 3:
+    if lat.q == 1 and lat.k_half == (1,) and lat.boundary == BOUNDARY_PERIODIC and lat.n_sites < 3:
         raise ConfigurationError("ring needs at least 3 sites")
+    if lat.n_sites > 2**31 - 1:
+        raise CapacityError("lattice too large for 32-bit site tables")
 
 
-def build_topology(space: JointSpace) -> RingStencil:
+def build_topology(space: JointSpace) -> LatticeStencil:
     check_supported(space)
-    return RingStencil(space=space)
+    return LatticeStencil(space=space)

@@ -55,32 +55,46 @@ class CouplingModel:
         return float(self.tunneling_per_direction(1)[0])
 
 
-def handle_for(m, n, onsite, tunneling, interaction, hbar, device=None):
-    """Cached ``native.Handle`` for a model on a device."""
+def handle_for(m, n, onsite, tunneling, interaction, hbar, device=None, lattice=None, lattice_key=None):
+    """Cached ``native.Handle`` for a model on a device (``lattice``: move
+    tables of a non-ring lattice, identified by ``lattice_key``)."""
     import torch
 
     from .native import Handle
 
     if device is None:
         device = torch.cuda.current_device() if torch.cuda.is_available() else 0
-    key = (int(m), int(n), float(onsite), float(tunneling), float(interaction), float(hbar), int(device))
+    key = (int(m), int(n), float(onsite), float(tunneling), float(interaction), float(hbar), int(device),
+           lattice_key)
     h = _HANDLES.get(key)
     if h is None:
-        h = Handle(m, n, onsite, tunneling, interaction, hbar, device)
+        h = Handle(m, n, onsite, tunneling, interaction, hbar, device, lattice=lattice)
         _HANDLES[key] = h
     return h
 
 
 def model_handle(topology, model: CouplingModel, hbar=None, device=None):
-    return handle_for(topology.m, topology.n, model.onsite_energy, model.ring_tunneling(),
-                      model.interaction, model.hbar if hbar is None else hbar, device)
+    """Handle for ``topology`` + ``model``: the ring as is, any other lattice
+    with its move tables and the tunnelling of each slot's direction
+    (slot_couplings, hamiltonian.py:92-97)."""
+    hb = model.hbar if hbar is None else hbar
+    if topology.is_ring:
+        return handle_for(topology.m, topology.n, model.onsite_energy, model.ring_tunneling(),
+                          model.interaction, hb, device)
+    lat = topology.lattice
+    pos, neg, directions = topology.move_tables()
+    t_slot = model.tunneling_per_direction(lat.q)[directions]
+    key = (lat.dims, lat.k_half, lat.boundary, tuple(float(v) for v in t_slot))
+    return handle_for(topology.m, topology.n, model.onsite_energy, float(t_slot[0]), model.interaction, hb,
+                      device, lattice=(pos, neg, t_slot), lattice_key=key)
 
 
 @dataclass
 class StencilValues:
-    """Per-realization couplings of the ring operator (device tensors).
+    """Per-realization couplings of the lattice operator (device tensors).
 
-    ``hop``: ``batch + (N,)`` float64, ``site``: same or None.  ``batch`` is
+    ``hop``: ``batch + (N*K,)`` float64 (link x*K + s), ``site``: ``batch +
+    (N,)`` or None.  ``batch`` is
     ``()`` for one Hamiltonian shared by every state, ``(B,)`` for a stack.
     """
 
@@ -114,6 +128,7 @@ def assemble_values(topology, model: CouplingModel, link_values=None, site_value
     h = model_handle(topology, model)
     dev = torch.device(f"cuda:{h.device}")
     n = topology.n
+    nl = topology.n_links
     has_link = link_values is not None and np.shape(link_values)[-1] != 0
     has_site = site_values is not None and np.shape(site_values)[-1] != 0
     batch = ()
@@ -124,18 +139,18 @@ def assemble_values(topology, model: CouplingModel, link_values=None, site_value
     count = int(np.prod(batch)) if batch else 1
     noise_cols = []
     if has_link:
-        if np.shape(link_values)[-1] != n:
-            raise ConfigurationError(f"link_values needs {n} entries per realization")
-        noise_cols.append(_device_array(link_values, dev).reshape(count, n))
+        if np.shape(link_values)[-1] != nl:
+            raise ConfigurationError(f"link_values needs {nl} entries per realization")
+        noise_cols.append(_device_array(link_values, dev).reshape(count, nl))
     if has_site:
         if np.shape(site_values)[-1] != n:
             raise ConfigurationError(f"site_values needs {n} entries per realization")
         noise_cols.append(_device_array(site_values, dev).reshape(count, n))
-    hop = torch.empty((count, n), dtype=torch.float64, device=dev)
+    hop = torch.empty((count, nl), dtype=torch.float64, device=dev)
     site = torch.empty((count, n), dtype=torch.float64, device=dev) if has_site else None
     noise = torch.cat(noise_cols, dim=1).contiguous() if noise_cols else None
-    h.build_coefficients(noise, count, n if has_link else 0, n if has_site else 0, hop, site)
-    hop = hop.reshape(batch + (n,))
+    h.build_coefficients(noise, count, nl if has_link else 0, n if has_site else 0, hop, site)
+    hop = hop.reshape(batch + (nl,))
     if site is not None:
         site = site.reshape(batch + (n,))
     return StencilValues(topology=topology, model=model, hop=hop, site=site)
@@ -163,10 +178,10 @@ def bind_values(h, values: StencilValues, count: int):
     if vb == () or vcount == 1 and count == 1:
         stride = 0
     elif vcount == count:
-        stride = values.topology.n
+        stride = values.topology.n_links
     else:
         raise ConfigurationError(f"values batch {vb} does not match {count} states")
-    hop = values.hop.reshape(-1, values.topology.n)
+    hop = values.hop.reshape(-1, values.topology.n_links)
     site = values.site.reshape(-1, values.topology.n) if values.site is not None else None
     h.bind(hop, site, vcount, stride)
 

@@ -12,6 +12,8 @@ import ctypes
 import os
 import threading
 
+import numpy as np
+
 from .errors import (
     CapacityError,
     ConfigurationError,
@@ -107,6 +109,8 @@ SIGNATURES = {
     "ctqw_kernel_timing": (ctypes.c_int, [_P, _I32]),
     "ctqw_kernel_time": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
     "ctqw_step_kernel": (ctypes.c_char_p, [_P]),
+    "ctqw_set_lattice": (ctypes.c_int, [_P, _I32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                        ctypes.POINTER(_D)]),
     "ctqw_telegraph_init": (ctypes.c_int, [_P, ctypes.c_uint64, _I64, _I64, ctypes.POINTER(_D), _I32, _I64,
                                            _I64, _D, _P]),
     "ctqw_telegraph_values": (ctypes.c_void_p, [_P]),
@@ -179,7 +183,10 @@ class Handle:
     """One ``ctqw_handle_t``: a model bound to a CUDA device."""
 
     def __init__(self, m: int, n_sites: int, onsite: float, tunneling: float,
-                 interaction: float, hbar: float, device: int = 0):
+                 interaction: float, hbar: float, device: int = 0, lattice=None):
+        """``lattice`` = (pos, neg, t_slot) move tables of a general lattice
+        ((N, K) int arrays, -1 off-lattice; (K,) tunnelling per slot), None
+        for the periodic nearest-neighbour ring."""
         import torch
 
         if not torch.cuda.is_available():
@@ -189,13 +196,21 @@ class Handle:
         self.m = int(m)
         self.n = int(n_sites)
         self.dim = self.n ** self.m
-        model = Model(self.m, self.n, 1, 1, float(onsite), float(tunneling), float(interaction),
-                      float(hbar))
+        self.K = 1 if lattice is None else int(np.shape(lattice[0])[1])
+        model = Model(self.m, self.n, self.K, 1 if lattice is None else 0, float(onsite), float(tunneling),
+                      float(interaction), float(hbar))
         h = _P()
         code = self.lib.ctqw_create(ctypes.byref(model), self.device, ctypes.byref(h))
         _raise_for(code, None)
         self._h = h
         self._bound = None  # keep coefficient tensors alive
+        if lattice is not None:
+            pos = np.ascontiguousarray(lattice[0], dtype=np.int32)
+            neg = np.ascontiguousarray(lattice[1], dtype=np.int32)
+            ts = np.ascontiguousarray(lattice[2], dtype=np.float64)
+            self._check(self.lib.ctqw_set_lattice(
+                self._h, self.K, pos.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                neg.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ts.ctypes.data_as(ctypes.POINTER(_D))))
 
     # -- lifecycle -------------------------------------------------------
     def close(self):

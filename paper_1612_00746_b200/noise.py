@@ -185,12 +185,16 @@ def init_process(spec: NoiseSpec, where, seed):
     if int(seed[0]) < 0 or int(seed[1]) < 0:
         raise ConfigurationError("seeds must be non-negative")
     if not spec.is_static:
+        from .geometry import site_move_tables
         from .native import Handle
 
-        n = max(lattice.n_sites, 3)
-        if counts[0] not in (0, n) or counts[1] not in (0, n):
-            raise ConfigurationError("the device telegraph process needs a ring (K = 1) lattice")
-        handle = Handle(1, n, 0.0, 1.0, 0.0, 1.0, _device())
+        n = lattice.n_sites
+        ring = lattice.q == 1 and lattice.k_half == (1,) and lattice.boundary == "periodic" and n >= 3
+        tables = None
+        if not ring:
+            pos, neg, _, _ = site_move_tables(lattice)
+            tables = (pos, neg, np.ones(pos.shape[1]))
+        handle = Handle(1, n, 0.0, 1.0, 0.0, 1.0, _device(), lattice=tables)
         handle.telegraph_init(int(seed[0]), int(seed[1]), 1, spec.levels, counts[0], counts[1], spec.rate)
         return TelegraphProcess(spec, counts[0], counts[1], handle)
     handle = handle_for(1, max(lattice.n_sites, 3), 0.0, 1.0, 0.0, 1.0)

@@ -244,6 +244,65 @@ def telegraph_fixture():
     np.savez_compressed(os.path.join(HERE, "telegraph.npz"), meta=json.dumps(meta), **arrays)
 
 
+def lattice_fixture():
+    """General lattices (q > 1, k_half > 1, open boundaries; hilbert.py:189-359):
+    apply / Taylor-4 / RK4 steps on noisy instances, and run() rows."""
+    rng = np.random.default_rng(4242)
+    arrays = {}
+    meta = {"steps": [], "runs": []}
+    cases = (
+        dict(dims=[3, 4], k_half=[1, 1], boundary="periodic", m=2, b=2, tunneling=1.0),
+        dict(dims=[8], k_half=[1], boundary="open", m=1, b=3, tunneling=1.0),
+        dict(dims=[7], k_half=[1], boundary="open", m=2, b=2, tunneling=0.9),
+        dict(dims=[9], k_half=[2], boundary="periodic", m=2, b=2, tunneling=1.1),
+        dict(dims=[4, 3], k_half=[1, 1], boundary="open", m=2, b=2, tunneling=[1.0, 0.7]),
+        dict(dims=[3, 3], k_half=[1, 1], boundary="periodic", m=3, b=1, tunneling=[0.8, 1.2]),
+        dict(dims=[3, 5], k_half=[1, 2], boundary="open", m=2, b=2, tunneling=[1.0, 0.6]),
+    )
+    for idx, c in enumerate(cases):
+        lat = build_lattice(c["dims"], k_half=c["k_half"], boundary=c["boundary"])
+        space = JointSpace(lattice=lat, m=c["m"])
+        topo = build_topology(space)
+        model = CouplingModel(onsite_energy=0.3, tunneling=c["tunneling"], interaction=0.6, hbar=1.1)
+        b, n, nl = c["b"], lat.n_sites, lat.n_sites * lat.moves_half
+        link = 0.3 * rng.normal(size=(b, nl))
+        site = 0.3 * rng.normal(size=(b, n))
+        values = assemble_values(topo, model, link_values=link, site_values=site)
+        psi = rng.normal(size=(b, space.dim)) + 1j * rng.normal(size=(b, space.dim))
+        psi /= np.linalg.norm(psi, axis=1, keepdims=True)
+        dt = 0.04
+        arrays[f"link{idx}"] = link
+        arrays[f"site{idx}"] = site
+        arrays[f"psi{idx}"] = psi
+        arrays[f"apply{idx}"] = apply_values(topo, values, psi)
+        arrays[f"taylor4_{idx}"] = step_taylor_values(topo, values, psi, dt, hbar=model.hbar, order=4)
+        arrays[f"rk4_{idx}"] = step_rk4_values(topo, values, psi, dt, hbar=model.hbar)
+        meta["steps"].append(dict(c, onsite=0.3, interaction=0.6, hbar=1.1, dt=dt))
+    runs = (
+        dict(dims=[3, 4], k_half=[1, 1], boundary="periodic", m=2, R=3, steps=20, post_rate=10, rate=0.0,
+             target="both", observables=None),
+        dict(dims=[10], k_half=[1], boundary="open", m=2, R=4, steps=24, post_rate=8, rate=0.5,
+             target="both", observables=None),
+        dict(dims=[11], k_half=[2], boundary="periodic", m=1, R=3, steps=30, post_rate=10, rate=0.0,
+             target="tunneling", observables=None),
+    )
+    for idx, c in enumerate(runs):
+        lat = build_lattice(c["dims"], k_half=c["k_half"], boundary=c["boundary"])
+        cfg = RunConfig(space=JointSpace(lattice=lat, m=c["m"]),
+                        model=CouplingModel(onsite_energy=0.1, tunneling=1.0, interaction=0.5),
+                        noise=NoiseSpec(target=c["target"], levels=(-0.1, 0.1), rate=c["rate"]),
+                        stepper=StepperConfig(backend="taylor", dt=0.05), realizations=c["R"], steps=c["steps"],
+                        post_rate=c["post_rate"], master_seed=1234, workers=1, precision="double",
+                        observables=c["observables"])
+        sinks = MemorySinks()
+        report = run(cfg, sinks)
+        arrays[f"run{idx}_rows"] = np.array([r[3] for r in sinks.rows], dtype=np.float64)
+        meta["runs"].append(dict(c, rows=[(r[0], r[1], r[2]) for r in sinks.rows],
+                                 observables_resolved=list(cfg.observables), switch_count=report.switch_count,
+                                 corrections=report.norm_corrections))
+    np.savez_compressed(os.path.join(HERE, "lattices.npz"), meta=json.dumps(meta), **arrays)
+
+
 def density_fixture():
     """Reference dense <rho>: accumulate_density on a random stack and the
     packed snapshots of a small run() (density.py:57-98)."""
@@ -272,7 +331,8 @@ if __name__ == "__main__":
     import sys as _sys
 
     only = _sys.argv[1:]
-    for fn in (noise_fixture, stencil_fixture, segment_fixture, run_fixture, telegraph_fixture, density_fixture):
+    for fn in (noise_fixture, stencil_fixture, segment_fixture, run_fixture, telegraph_fixture, density_fixture,
+               lattice_fixture):
         if not only or fn.__name__ in only:
             fn()
     for f in sorted(os.listdir(HERE)):

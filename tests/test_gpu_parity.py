@@ -653,3 +653,43 @@ def test_run_dense_snapshots_match_reference(pkg):
         np.testing.assert_allclose(d.packed, data[f"snap{i}"], rtol=0, atol=1e-13)
         assert d.purity == pytest.approx(float(2 * np.sum(np.abs(data[f"snap{i}"]) ** 2)
                                                - np.sum(np.abs(np.diagonal(d.dense())) ** 2)), rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# general lattices (q > 1, k_half > 1, open boundaries): generic kernels
+
+
+@pytest.mark.parametrize("idx", range(7))
+def test_lattice_steps_bit_exact_vs_reference(pkg, idx):
+    p = pkg
+    data, meta = load_golden("lattices.npz")
+    c = meta["steps"][idx]
+    lat = p.build_lattice(c["dims"], k_half=c["k_half"], boundary=c["boundary"])
+    topo = p.build_topology(p.JointSpace(lat, c["m"]))
+    model = p.CouplingModel(onsite_energy=c["onsite"], tunneling=c["tunneling"], interaction=c["interaction"],
+                            hbar=c["hbar"])
+    values = p.assemble_values(topo, model, link_values=data[f"link{idx}"], site_values=data[f"site{idx}"])
+    psi = data[f"psi{idx}"]
+    np.testing.assert_array_equal(p.apply_values(topo, values, psi), data[f"apply{idx}"])
+    np.testing.assert_array_equal(p.step_taylor_values(topo, values, psi, c["dt"], hbar=c["hbar"], order=4),
+                                  data[f"taylor4_{idx}"])
+    np.testing.assert_array_equal(p.step_rk4_values(topo, values, psi, c["dt"], hbar=c["hbar"]), data[f"rk4_{idx}"])
+
+
+@pytest.mark.parametrize("idx", range(3))
+def test_lattice_run_rows_match_reference(pkg, idx):
+    p = pkg
+    data, meta = load_golden("lattices.npz")
+    c = meta["runs"][idx]
+    lat = p.build_lattice(c["dims"], k_half=c["k_half"], boundary=c["boundary"])
+    cfg = p.RunConfig(space=p.JointSpace(lat, c["m"]),
+                      model=p.CouplingModel(onsite_energy=0.1, tunneling=1.0, interaction=0.5),
+                      noise=p.NoiseSpec(target=c["target"], levels=(-0.1, 0.1), rate=c["rate"]),
+                      stepper=p.StepperConfig(backend="taylor", dt=0.05), realizations=c["R"], steps=c["steps"],
+                      post_rate=c["post_rate"], master_seed=1234, precision="double")
+    sinks = p.MemorySinks()
+    report = p.run(cfg, sinks)
+    assert [(t, n, i) for t, n, i, _ in sinks.rows] == [tuple(r) for r in c["rows"]]
+    np.testing.assert_allclose([v for *_, v in sinks.rows], data[f"run{idx}_rows"], rtol=1e-10, atol=1e-13)
+    assert report.switch_count == c["switch_count"]
+    assert report.norm_corrections == c["corrections"]

@@ -87,12 +87,25 @@ def test_default_observables_and_position_rule():
 
 def test_topology_scope():
     assert p.build_topology(ring(7, 2)).dim == 49
-    with pytest.raises(p.ConfigurationError):
-        p.build_topology(p.JointSpace(p.build_lattice([3, 4]), 2))
-    with pytest.raises(p.ConfigurationError):
-        p.build_topology(p.JointSpace(p.build_lattice([8], boundary="open"), 1))
+    assert p.build_topology(ring(7, 2)).is_ring
+    grid = p.build_topology(p.JointSpace(p.build_lattice([3, 4]), 2))
+    assert not grid.is_ring and grid.K == 2 and grid.n_links == 24
+    chain = p.build_topology(p.JointSpace(p.build_lattice([8], boundary="open"), 1))
+    pos, neg, _ = chain.move_tables()
+    assert pos[7, 0] == -1 and neg[0, 0] == -1 and pos[3, 0] == 4
     with pytest.raises(p.ConfigurationError):
         p.build_topology(ring(5, 4))
+
+
+def test_site_move_tables_match_reference_convention():
+    """Slots direction-major, distance 1..k_half (hilbert.py:189-224)."""
+    lat = p.build_lattice([4, 5], k_half=[1, 2])
+    pos, neg, dirs, dist = p.site_move_tables(lat)
+    assert list(dirs) == [0, 1, 1] and list(dist) == [1, 1, 2]
+    # site (1, 3) = 8: +x0 -> (2, 3) = 13, +x1 by 2 -> (1, 0) = 5 (periodic)
+    assert pos[8, 0] == 13 and pos[8, 2] == 5 and neg[8, 1] == 7
+    for s in range(3):  # mirror pairing: neg undoes pos
+        assert all(neg[pos[x, s], s] == x for x in range(lat.n_sites))
 
 
 def test_initial_states():
@@ -176,7 +189,9 @@ def test_handle_create_errors_without_device():
     h = ctypes.c_void_p()
     bad = native.Model(4, 16, 1, 1, 0.0, 1.0, 0.0, 1.0)
     assert lib.ctqw_create(ctypes.byref(bad), 0, ctypes.byref(h)) == 2
-    bad = native.Model(2, 16, 2, 1, 0.0, 1.0, 0.0, 1.0)
+    bad = native.Model(2, 16, 0, 1, 0.0, 1.0, 0.0, 1.0)  # no move slots
+    assert lib.ctqw_create(ctypes.byref(bad), 0, ctypes.byref(h)) == 2
+    bad = native.Model(2, 1, 1, 0, 0.0, 1.0, 0.0, 1.0)  # one-site lattice
     assert lib.ctqw_create(ctypes.byref(bad), 0, ctypes.byref(h)) == 2
     bad = native.Model(2, 16, 1, 1, 0.0, 1.0, 0.0, -1.0)
     assert lib.ctqw_create(ctypes.byref(bad), 0, ctypes.byref(h)) == 2

@@ -161,3 +161,47 @@ def test_run_rows_dynamic_noise(idx):
     np.testing.assert_allclose([v for *_, v in rows], data[f"run{idx}_rows"], rtol=1e-10, atol=1e-13)
     assert int(tg.switches.sum()) == c["switch_count"]
     assert totals.corrections == c["corrections"]
+
+
+# ---------------------------------------------------------------------------
+# general lattices (q > 1, k_half > 1, open boundaries)
+
+
+@pytest.mark.parametrize("idx", range(7))
+def test_lattice_steps_match_reference(idx):
+    data, meta = load_golden("lattices.npz")
+    c = meta["steps"][idx]
+    st = orc.make_lattice_stencil(c["m"], c["dims"], c["k_half"], c["boundary"], c["onsite"], c["tunneling"],
+                                  c["interaction"], link=data[f"link{idx}"], site=data[f"site{idx}"],
+                                  batch=c["b"])
+    psi = data[f"psi{idx}"]
+    np.testing.assert_array_equal(orc.apply_stencil(st, psi), data[f"apply{idx}"])
+    np.testing.assert_array_equal(orc.taylor_step(st, psi, c["dt"], c["hbar"], 4), data[f"taylor4_{idx}"])
+    np.testing.assert_array_equal(orc.rk4_step(st, psi, c["dt"], c["hbar"]), data[f"rk4_{idx}"])
+
+
+@pytest.mark.parametrize("idx", range(3))
+def test_lattice_run_rows(idx):
+    from oracle.noise_oracle import TelegraphOracle
+
+    data, meta = load_golden("lattices.npz")
+    c = meta["runs"][idx]
+    n = int(np.prod(c["dims"]))
+    K = sum(c["k_half"])
+    nl = n * K if c["target"] in ("tunneling", "both") else 0
+    ns = n if c["target"] in ("onsite", "both") else 0
+    if c["rate"] > 0:
+        tg = TelegraphOracle(1234, 0, c["R"], (-0.1, 0.1), nl, ns, c["rate"])
+        noise = tg.values
+    else:
+        tg = None
+        noise = np.stack([draw_static_noise(1234, r, (-0.1, 0.1), nl + ns) for r in range(c["R"])])
+    st = orc.make_lattice_stencil(c["m"], c["dims"], c["k_half"], c["boundary"], 0.1, 1.0, 0.5,
+                                  link=noise[:, :nl] if nl else None, site=noise[:, nl:].copy() if ns else None,
+                                  batch=c["R"])
+    out, _, totals = orc.run_rows(st, orc.product_state(c["m"], n), c["R"], c["steps"], c["post_rate"], 0.05,
+                                  observables=c["observables_resolved"], noise=tg, tunneling=1.0,
+                                  periodic=c["boundary"] == "periodic")
+    rows = [(t, name, i, v) for t, rr in out for name, i, v in rr]
+    assert [(t, nm, i) for t, nm, i, _ in rows] == [tuple(r) for r in c["rows"]]
+    np.testing.assert_allclose([v for *_, v in rows], data[f"run{idx}_rows"], rtol=1e-10, atol=1e-13)
