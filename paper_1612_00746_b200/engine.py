@@ -434,7 +434,7 @@ def _dense_snapshot(config, ens, group, time_tag):
         part = packed_density_device(ens.states(), ens.count) * ens.count
     else:
         part = torch.zeros(packed_length(dim), dtype=torch.complex128, device=ens.dev)
-    if group is not None and sharding.world_info(group)[1] > 1:
+    if group is not None and sharding._collective(group):
         import torch.distributed as dist
 
         real = torch.view_as_real(part).contiguous()

@@ -17,6 +17,18 @@ the multi-process logic is tested without GPUs.
 from __future__ import annotations
 
 
+def _collective(group=None) -> bool:
+    """Run the collectives?  Yes on more than one rank; also on one rank when
+    CTQW_FORCE_COLLECTIVES=1 (exercises the NCCL path on a single-GPU box)."""
+    import os
+
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return False
+    return dist.get_world_size(group) > 1 or os.environ.get("CTQW_FORCE_COLLECTIVES") == "1"
+
+
 def world_info(group=None):
     import torch.distributed as dist
 
@@ -41,7 +53,7 @@ def allreduce_sum_(tensor, group=None):
     """In-place sum over ranks (no-op on one rank)."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if _collective(group):
         dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
     return tensor
 
@@ -50,7 +62,7 @@ def gather_objects(obj, group=None):
     """List of ``obj`` from every rank in rank order."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if _collective(group):
         out = [None] * dist.get_world_size(group)
         dist.all_gather_object(out, obj, group=group)
         return out
@@ -84,7 +96,7 @@ def gather_states(local, group=None):
     import torch
     import torch.distributed as dist
 
-    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+    if not _collective(group):
         return local
     sizes = gather_objects(int(local.shape[0]), group)
     flat = torch.view_as_real(local) if local.is_complex() else local

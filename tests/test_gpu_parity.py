@@ -693,3 +693,41 @@ def test_lattice_run_rows_match_reference(pkg, idx):
     np.testing.assert_allclose([v for *_, v in sinks.rows], data[f"run{idx}_rows"], rtol=1e-10, atol=1e-13)
     assert report.switch_count == c["switch_count"]
     assert report.norm_corrections == c["corrections"]
+
+
+# ---------------------------------------------------------------------------
+# NCCL plumbing on the real device (one rank: the box has one GPU)
+
+
+def test_run_through_nccl_group_matches_single_process(pkg, monkeypatch):
+    """run(config, group=<NCCL world of 1>) goes through the NCCL all-reduce of
+    the diagonal partials, the object gathers of the norm statistics and the
+    state gather for purity; rows equal the group-less run bit for bit."""
+    import socket
+
+    import torch.distributed as dist
+
+    p = pkg
+    monkeypatch.setenv("CTQW_FORCE_COLLECTIVES", "1")  # run the NCCL calls even on one rank
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([24]), 2),
+                          model=p.CouplingModel(onsite_energy=0.1, interaction=0.3),
+                          noise=p.NoiseSpec(target="both", rate=0.3), stepper=p.StepperConfig(dt=0.05),
+                          realizations=5, steps=20, post_rate=5, precision="double",
+                          observables=("populations", "position_mean_variance", "purity", "participation_ratio"))
+        a, b = p.MemorySinks(), p.MemorySinks(dense=True)
+        ra = p.run(cfg, a, group=dist.group.WORLD)
+        p.run(cfg, b, group=dist.group.WORLD)
+        plain = p.MemorySinks()
+        rp = p.run(cfg, plain)
+        assert a.rows == plain.rows
+        assert ra.switch_count == rp.switch_count and ra.norm_corrections == rp.norm_corrections
+        np.testing.assert_allclose(b.densities[-1].diagonal().real, plain.densities[-1].diag, rtol=1e-12, atol=1e-15)
+    finally:
+        dist.destroy_process_group()
