@@ -52,6 +52,8 @@ struct ctqw_ctx {
   Summary* summary_dev = nullptr;
   Summary* summary_host = nullptr;
   double2* scratch[2] = {nullptr, nullptr};
+  double2* scratch_work = nullptr;  // second state buffer when the caller passes none
+  int64_t scratch_work_elems = 0;
   int64_t scratch_elems = 0;
   double* n2_dev = nullptr;
   int64_t n2_cap = 0;
@@ -375,7 +377,7 @@ int ctqw_destroy(ctqw_handle_t h) {
   void* dev_ptrs[] = {h->levels, h->partial, h->scl, h->stats, h->events, h->fail,
                       h->summary_dev, h->scratch[0], h->scratch[1], h->n2_dev, h->small,
                       h->overlap_partial, h->tg_values, h->tg_next, h->tg_gen, h->tg_levels, h->tg_sum,
-                      h->lat_pos, h->lat_neg, h->t_slot};
+                      h->lat_pos, h->lat_neg, h->t_slot, h->scratch_work};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (h->summary_host) cudaFreeHost(h->summary_host);
@@ -703,7 +705,23 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
     }
     return CTQW_OK;
   }
-  if (!work) return fail_with(h, CTQW_ERR_CONFIG, "work buffer required");
+  // plane3 (m = 3, N = 128) updates psi in place; every other streaming or
+  // generic path needs a second buffer: the caller's, or (work NULL / aliased
+  // to psi) a library-owned one
+  const bool plane3_path = (h->stream_kind == 0 || h->stream_kind == 5) && !h->general &&
+                           plane3_supported(h->m, h->n, sc);
+  if (!plane3_path && (!work || work == psi)) {
+    if (!h->scratch_work || h->scratch_work_elems < count * h->dim) {
+      if (h->scratch_work) cudaFree(h->scratch_work);
+      h->scratch_work = nullptr;
+      h->scratch_work_elems = 0;
+      if (cudaMalloc((void**)&h->scratch_work, (size_t)count * h->dim * sizeof(double2)) != cudaSuccess)
+        return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate the second state buffer");
+      h->scratch_work_elems = count * h->dim;
+    }
+    work = h->scratch_work;
+  }
+  if (!work) work = psi;
   // streaming m = 2 path: the four-column band kernel by default; the older
   // band / band2 / tile kernels stay selectable for A/B measurements
   // CTQW_STREAM pins one kernel family (A/B measurements, per-kernel parity
@@ -726,7 +744,8 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
                                   : tile_parts(h->n, sc);
     rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
     if (rc) return rc;
-    double2* bufs[2] = {psi, work};
+    // plane3 marches in place (output planes 0..3 parked until the march ends)
+    double2* bufs[2] = {psi, use_plane3 ? psi : work};
     for (int64_t j = 0; j < n_steps; ++j) {
       const double2* in = bufs[j & 1];
       double2* out = bufs[(j + 1) & 1];
@@ -754,9 +773,14 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       if (rc) return rc;
     }
     double2* final_buf = bufs[n_steps & 1];
+    if (final_buf != psi && final_buf == h->scratch_work) {  // library-owned second buffer: result back to psi
+      CUDA_TRY(h, cudaMemcpyAsync(psi, final_buf, (size_t)count * h->dim * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, s));
+      final_buf = psi;
+    }
     CUDA_TRY(h, launch_rescale(final_buf, count, h->dim, h->scl, s));
     h->launches += 2;
-    if (result_in_work) *result_in_work = (int32_t)(n_steps & 1);
+    if (result_in_work) *result_in_work = final_buf == psi ? 0 : 1;
     return CTQW_OK;
   }
   // generic path: in place on psi; work = term buffer A, library scratch B, C

@@ -50,11 +50,14 @@ constexpr int kThreads3 = 256;       // 4 x1 pairs x 64 x2 pairs
 constexpr int kPB = 16;              // planes per norm block
 constexpr int kNblk3 = kN3 / kPB;    // norm blocks per realization per CTA
 constexpr int kRowB = kN3 * 16;      // bytes per x1 row (128 complex)
+constexpr int kWrap = 4;             // planes re-read at the end of a full-ring march (NAPP)
 constexpr int kPlaneB = kTR * kRowB; // ring bytes per plane
 
 struct Plane3Args {
   CUtensorMap tmap;  // psi_in: (16 doubles, 16 lines, x1, count*N planes), box = one x1 row
   double2* psi_out;
+  double2* side;     // in place: [cluster][kWrap][N][N] output planes 0..kWrap-1 parked until the end
+  int inplace;       // psi_out == psi_in
   int64_t count;
   Coef coef;
   StencilConst k;
@@ -124,6 +127,7 @@ __device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
 
 struct Piece3 {
   double2* dst;
+  double2* side;  // parked planes (in place), else nullptr
   double* part;
   int64_t g0;  // plane coordinate of x0 = 0 for this realization (r * N)
   int j0, ya, yb, last_rho;
@@ -264,7 +268,10 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
 }
 
 __device__ __forceinline__ void store3(const T3& T, Piece3& P, int rr, const Quad& o, double& nrm) {
-  double2* base = P.dst + ((int64_t)rr * kN3 + T.x1a) * kN3 + T.x2a;
+  // in place, output planes 0..kWrap-1 would overwrite psi planes the march
+  // reads again at its end (as planes N..N+3): park them
+  double2* base = (P.side && rr < kWrap) ? P.side + ((int64_t)rr * kN3 + T.x1a) * kN3 + T.x2a
+                                         : P.dst + ((int64_t)rr * kN3 + T.x1a) * kN3 + T.x2a;
   st256b(base, o.c[0], o.c[1]);
   st256b(base + kN3, o.c[2], o.c[3]);
 #pragma unroll
@@ -478,12 +485,19 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_addr(q)), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // the cluster's run of (realization, x0 block) work items
+  // the cluster's run of (realization, x0 block) work items; in place, whole
+  // realizations only (a split realization would overwrite another piece's halo)
   const int64_t nclus = gridDim.x / kCl;
   const int64_t gid = blockIdx.x / kCl;
   const int64_t total = a.count * kNblk3;
-  int64_t lo = total * gid / nclus;
-  const int64_t hi = total * (gid + 1) / nclus;
+  int64_t lo, hi;
+  if (a.inplace) {
+    lo = (a.count * gid / nclus) * kNblk3;
+    hi = (a.count * (gid + 1) / nclus) * kNblk3;
+  } else {
+    lo = total * gid / nclus;
+    hi = total * (gid + 1) / nclus;
+  }
   double2* hop2 = smem3 + kHopOff;
   double* site = site_tab();
   constexpr int64_t dim = (int64_t)kN3 * kN3 * kN3;
@@ -509,6 +523,7 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     P.s = a.scl ? a.scl[r] : 1.0;
     P.scale = P.s != 1.0;
     P.dst = a.psi_out + r * dim;
+    P.side = a.inplace ? a.side + gid * (int64_t)kWrap * kN3 * kN3 : nullptr;
     P.part = a.partial + r * (kNblk3 * kCl);
     P.g0 = r * kN3;
     P.pend = -1;
@@ -536,6 +551,18 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     cluster_wait();   // completes the last iteration's arrive
     __syncthreads();  // the last stage has written its norm partials
     flush3(T, P, true);
+    if (P.side) {
+      // every CTA has read planes 0..kWrap-1 (its band and halo rows) for the
+      // last time: move the parked output planes in; each thread copies the
+      // elements it parked itself, so program order suffices
+      cluster_sync_all();
+      for (int pl = 0; pl < kWrap; ++pl)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t off = ((int64_t)pl * kN3 + T.x1a + (q >> 1)) * kN3 + T.x2a + (q & 1);
+          P.dst[off] = P.side[off];
+        }
+    }
   }
   cluster_sync_all();  // no CTA leaves while a neighbour may still read its exchange planes
 }
@@ -573,6 +600,25 @@ cudaError_t encode_planes_map(CUtensorMap* map, const double2* base, int64_t cou
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Parking space for the in-place march: kWrap planes per cluster, per device.
+double2* side_buffer(int nclus) {
+  static double2* buf[64] = {};
+  static int cap[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (nclus > cap[dev]) {
+    if (buf[dev]) cudaFree(buf[dev]);
+    buf[dev] = nullptr;
+    cap[dev] = 0;
+    if (cudaMalloc(&buf[dev], (size_t)nclus * kWrap * kN3 * kN3 * sizeof(double2)) != cudaSuccess) return nullptr;
+    cap[dev] = nclus;
+  }
+  return buf[dev];
+}
+
 template <int NAPP, bool RK4, bool SITE, bool EXACT>
 cudaError_t launch_p3(Plane3Args a, const double2* psi_in, cudaStream_t s) {
   auto kern = plane3_kernel<NAPP, RK4, SITE, EXACT>;
@@ -601,8 +647,12 @@ cudaError_t launch_p3(Plane3Args a, const double2* psi_in, cudaStream_t s) {
   }
   cudaError_t e = encode_planes_map(&a.tmap, psi_in, a.count);
   if (e != cudaSuccess) return e;
-  const int64_t work = a.count * kNblk3;
+  const int64_t work = a.inplace ? a.count : a.count * kNblk3;
   const int64_t clusters = std::min<int64_t>(nclus, work);
+  if (a.inplace) {
+    a.side = side_buffer((int)clusters);
+    if (!a.side) return cudaErrorMemoryAllocation;
+  }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -632,6 +682,8 @@ cudaError_t launch_plane3_step(const double2* psi_in, double2* psi_out, int64_t 
   if (count == 0) return cudaSuccess;
   Plane3Args a;
   a.psi_out = psi_out;
+  a.inplace = psi_out == psi_in ? 1 : 0;
+  a.side = nullptr;
   a.count = count;
   a.coef = coef;
   a.k = k;

@@ -222,16 +222,27 @@ def estimate_memory(config: RunConfig, world: int = 1) -> dict:
     n = space.lattice.n_sites
     r_local = -(-config.realizations // world)
     state = r_local * dim * 16
-    coeff = r_local * n * 8 * 3
+    buffers = 1 if marches_in_place(config) else 2
+    coeff = r_local * n * 8 * (2 + space.lattice.moves_half)
     return {
         "joint_dim": dim,
         "itemsize": 16,
-        "state_bytes": 2 * state,
+        "state_bytes": buffers * state,
         "hamiltonian_bytes": coeff,
         "topology_bytes": 0,
         "density_bytes": dim * 8 * 2,
-        "total_bytes": 2 * state + coeff + dim * 16,
+        "total_bytes": buffers * state + coeff + dim * 16,
     }
+
+
+def marches_in_place(config: RunConfig) -> bool:
+    """The m = 3, N = 128 cluster kernel updates the states in place (one
+    buffer, so twice the realizations per GPU -- configs[4])."""
+    lat = config.space.lattice
+    st = config.stepper
+    return (config.space.m == 3 and lat.q == 1 and lat.k_half == (1,) and lat.boundary == "periodic"
+            and lat.n_sites == 128 and (st.backend == "rk4" or st.taylor_order == 4)
+            and os.environ.get("CTQW_STREAM", "") in ("", "plane3"))
 
 
 class OutputSinks:
@@ -364,7 +375,9 @@ class EnsembleState:
         psi0 = build_initial_state(config.initial, space)
         self.psi0 = torch.as_tensor(psi0, device=self.dev)
         self.psi = torch.empty((max(self.count, 1), space.dim), dtype=torch.complex128, device=self.dev)
-        self.work = torch.empty_like(self.psi)
+        # one buffer when the step kernel marches in place (the library keeps a
+        # second one itself if another path ends up running)
+        self.work = self.psi if marches_in_place(config) else torch.empty_like(self.psi)
         if self.count:
             self.handle.fill_states(self.psi, self.count, self.psi0)
         self.stepper = config.stepper.native(config.exact)
@@ -376,7 +389,7 @@ class EnsembleState:
             return
         swapped = self.handle.evolve(self.psi, self.work, self.count, first_step, n_steps,
                                      self.stepper)
-        if swapped:
+        if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
 
     def stats(self) -> dict:

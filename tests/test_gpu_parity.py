@@ -731,3 +731,28 @@ def test_run_through_nccl_group_matches_single_process(pkg, monkeypatch):
         np.testing.assert_allclose(b.densities[-1].diagonal().real, plain.densities[-1].diag, rtol=1e-12, atol=1e-15)
     finally:
         dist.destroy_process_group()
+
+
+def test_evolve_without_second_buffer(pkg):
+    """work aliased to psi on a path that needs two buffers: the library uses
+    its own second buffer and returns the result in psi."""
+    B, n = 3, 96
+    h, st, _keep = device_case(2, n, B, "both")
+    psi0 = np.tile(orc.product_state(2, n), (B, 1))
+    psi = to_dev(psi0)
+    swapped = h.evolve(psi, psi, B, 0, 7, stepper(dt=0.05))
+    assert not swapped
+    ref, _ = orc.evolve_segment(st, psi0.copy(), 0, 7, 0.05)
+    assert np.abs(psi.cpu().numpy() - ref).max() <= 1e-13
+
+
+def test_plane3_in_place_run_capacity(pkg):
+    """configs[4] marches in place: one state buffer per realization."""
+    p = pkg
+    from paper_1612_00746_b200.engine import estimate_memory, marches_in_place
+
+    cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([128]), 3), noise=p.NoiseSpec(rate=0.0),
+                      stepper=p.StepperConfig(dt=0.015), realizations=5000, steps=1, post_rate=1,
+                      precision="double", memory_budget=200 * 2**30)
+    assert marches_in_place(cfg)
+    assert estimate_memory(cfg)["state_bytes"] == 5000 * 2**21 * 16
