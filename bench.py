@@ -301,10 +301,13 @@ def ours(a):
     from paper_1612_00746_b200 import engine, sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    # launched by torchrun: one process per GPU over NCCL (also at world 1, so
+    # the distributed path -- barriers, MAX reductions, run(group=...) -- runs)
+    distributed = "RANK" in os.environ and "MASTER_ADDR" in os.environ
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     R_total = a.realizations * world
     obs = ("populations", "position_mean_variance", "participation_ratio")
@@ -319,7 +322,7 @@ def ours(a):
     dim = a.n ** a.m
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     # warm-up (includes one collection point)
@@ -363,7 +366,7 @@ def ours(a):
     ms_other = start.elapsed_time(stop)
     ens.stepper = cfg.stepper.native(bool(a.exact))
     t = torch.tensor([ms, ms_other], device=f"cuda:{local}")
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_other_max = float(t[1].item())
     ms_max = float(t[0].item())
@@ -398,10 +401,10 @@ def ours(a):
         sinks = p.MemorySinks(keep_densities=False)
         barrier()
         t0 = time.perf_counter()
-        p.run(cfg, sinks, group=None if world == 1 else dist.group.WORLD)
+        p.run(cfg, sinks, group=dist.group.WORLD if distributed else None)
         torch.cuda.synchronize()
         t_e2e = torch.tensor([time.perf_counter() - t0], device=f"cuda:{local}")
-        if world > 1:
+        if distributed:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         e2e_s = float(t_e2e.item())
         h2d = dim * 16 + 16  # initial state + noise levels
@@ -434,7 +437,7 @@ def ours(a):
             "norm_events": stats["event_count"],
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
