@@ -1,6 +1,7 @@
 // Internal launch interface between api.cu and the kernel translation units.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -9,6 +10,23 @@
 namespace ctqw {
 
 constexpr int64_t kMaxGridY = 65535;
+
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// Once-per-device flag: function attributes (cudaFuncSetAttribute) belong to
+// a device, and one process may drive a handle per GPU.
+struct DeviceOnce {
+  std::atomic<uint64_t> done{0};
+  bool first() {
+    const int d = current_device() & 63;
+    const uint64_t bit = 1ull << d;
+    return !(done.fetch_or(bit) & bit);
+  }
+};
 constexpr int kMaxParts = 256;  // norm partials per realization
 
 // Diagonal base per coincidence count c: m*eps0 + U*c (hamiltonian.py:132).

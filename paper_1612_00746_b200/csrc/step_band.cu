@@ -742,12 +742,11 @@ BandPlan plan_band(int n, int napp, bool site, int64_t count, int num_sms) {
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool FULL, int MAXT>
 cudaError_t launch_band_t(const BandArgs& args, const BandPlan& p, int64_t count, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce once;
+  if (once.first()) {
     cudaError_t e = cudaFuncSetAttribute(band_step_kernel<NAPP, RK4, SITE, EXACT, FULL, MAXT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   BandArgs a = args;
   for (int64_t r0 = 0; r0 < count; r0 += kMaxGridY) {
@@ -761,12 +760,11 @@ cudaError_t launch_band_t(const BandArgs& args, const BandPlan& p, int64_t count
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool FULL>
 cudaError_t launch_ws_t(const BandArgs& args, const BandPlan& p, int64_t count, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce once;
+  if (once.first()) {
     cudaError_t e = cudaFuncSetAttribute(band_ws_kernel<NAPP, RK4, SITE, EXACT, FULL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   BandArgs a = args;
   for (int64_t r0 = 0; r0 < count; r0 += kMaxGridY) {

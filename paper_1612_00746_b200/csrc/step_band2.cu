@@ -424,12 +424,11 @@ Band2Plan plan_band2(int n, int napp, bool site, int64_t count, int num_sms) {
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool FULL>
 cudaError_t launch_b2(const Band2Args& args, const Band2Plan& p, int64_t count, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce once;
+  if (once.first()) {
     cudaError_t e = cudaFuncSetAttribute(band2_kernel<NAPP, RK4, SITE, EXACT, FULL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   Band2Args a = args;
   for (int64_t r0 = 0; r0 < count; r0 += kMaxGridY) {

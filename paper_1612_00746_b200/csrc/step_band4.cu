@@ -654,8 +654,8 @@ cudaError_t encode_rows_map(CUtensorMap* map, const double2* base, int n, int64_
 template <int NAPP, bool RK4, bool SITE, bool EXACT, int NN>
 cudaError_t launch_b4(const Band4Args& args, Band4Plan p, cudaStream_t s) {
   auto kern = band4_kernel<NAPP, RK4, SITE, EXACT, NN>;
-  static int per_sm = 0;
-  if (per_sm == 0) {
+  static DeviceOnce once;
+  if (once.first()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
   }
@@ -663,7 +663,6 @@ cudaError_t launch_b4(const Band4Args& args, Band4Plan p, cudaStream_t s) {
   int occ = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, p.threads, p.smem);
   if (e != cudaSuccess) return e;
-  per_sm = occ;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int64_t slots = (int64_t)occ * sm_count4();
   const int64_t grid = std::min<int64_t>(slots, args.count * p.nblk);

@@ -622,7 +622,8 @@ double2* side_buffer(int nclus) {
 template <int NAPP, bool RK4, bool SITE, bool EXACT>
 cudaError_t launch_p3(Plane3Args a, const double2* psi_in, cudaStream_t s) {
   auto kern = plane3_kernel<NAPP, RK4, SITE, EXACT>;
-  static int nclus = 0;
+  static int nclus_dev[64] = {};
+  int& nclus = nclus_dev[current_device() & 63];
   if (nclus == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem3);
     if (e != cudaSuccess) return e;

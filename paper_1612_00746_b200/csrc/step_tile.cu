@@ -353,12 +353,11 @@ __global__ void __launch_bounds__(512, 1) resident_kernel(ResArgs a) {
 template <bool RK4, bool SITE, bool EXACT>
 cudaError_t launch_tile_t(const TileArgs& args, int64_t count, cudaStream_t s) {
   constexpr size_t smem = tile_smem_bytes<RK4>();
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce once;
+  if (once.first()) {
     cudaError_t e = cudaFuncSetAttribute(tile_step_kernel<RK4, SITE, EXACT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   TileArgs a = args;
   for (int64_t r0 = 0; r0 < count; r0 += kMaxGridY) {
@@ -382,13 +381,12 @@ template <bool RK4, bool SITE, bool EXACT>
 cudaError_t launch_res_t(const ResArgs& args, int64_t count, cudaStream_t s) {
   const int n = args.n;
   const size_t smem = (size_t)n * n * sizeof(double2) * (RK4 ? 2 : 1) + (size_t)(2 * n + 32) * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce once;
+  if (once.first()) {
     const int maxs = kResidentMax * kResidentMax * (int)sizeof(double2) * 2 + (2 * kResidentMax + 32) * 8;
     cudaError_t e = cudaFuncSetAttribute(resident_kernel<RK4, SITE, EXACT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   const int threads = ((n + kSR - 1) / kSR) * n;
   ResArgs a = args;

@@ -168,12 +168,13 @@ cudaError_t launch_telegraph_advance(int64_t count, int64_t total, int64_t n_lin
                                      int64_t site_stride, const long long* fail, cudaStream_t s) {
   if (count <= 0 || total <= 0) return cudaSuccess;
   const size_t smem = telegraph_advance_smem(total);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  static size_t configured[64] = {};
+  size_t& conf = configured[current_device() & 63];
+  if (smem > 48 * 1024 && smem > conf) {
     cudaError_t e = cudaFuncSetAttribute(telegraph_advance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    conf = smem;
   }
   telegraph_advance_kernel<<<(unsigned)((count + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps, smem, s>>>(
       count, total, n_links, n_sites, n, dt, levels_dev, n_levels, mean_wait, t_slot, K, values, next_switch, gen,
