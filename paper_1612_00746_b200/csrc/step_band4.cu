@@ -155,7 +155,13 @@ struct T4 {
   int offl, offr;     // swizzled ring offsets of columns 4p-1 and 4p+4
   const double* colc; // smem column couplings: [q][NP] hop[4p+q] (q < 4), hop[4p-1] (q = 4), site[4p+q] (5..8)
   int NP;
+  double hc[kCols];   // register copy of the column couplings (kColcRegs)
+  double hm0;
 };
+
+// Column tunnelling couplings: in registers (10 registers, no loads) for the
+// Taylor kernels, re-read from shared memory per application for RK4 (which
+// carries one more row and would spill).
 
 // Column couplings of the thread's four columns, re-read from shared memory
 // at every stencil application (holding them in registers spills).
@@ -165,12 +171,18 @@ struct ColC {
   double sx[kCols];   // site[x]
 };
 
-template <bool SITE>
+template <bool SITE, bool CREG>
 __device__ __forceinline__ ColC load_colc(const T4& T) {
   ColC c;
+  if (CREG) {
 #pragma unroll
-  for (int q = 0; q < kCols; ++q) c.hc[q] = T.colc[q * T.NP + T.p];
-  c.hm0 = T.colc[kCols * T.NP + T.p];
+    for (int q = 0; q < kCols; ++q) c.hc[q] = T.hc[q];
+    c.hm0 = T.hm0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kCols; ++q) c.hc[q] = T.colc[q * T.NP + T.p];
+    c.hm0 = T.colc[kCols * T.NP + T.p];
+  }
 #pragma unroll
   for (int q = 0; q < kCols; ++q) c.sx[q] = SITE ? T.colc[(kCols + 1 + q) * T.NP + T.p] : 0.0;
   return c;
@@ -243,13 +255,13 @@ __device__ __forceinline__ Row4 ring_row(const Geo4<NN>& g, const T4& T, int slo
 // (H z)(r, x) for the thread's four columns of row r: up = row r-1,
 // mid = row r, dn = row r+1, lf / rt = columns 4p-1 / 4p+4 of row r.
 // DG: the diagonal carries the coincidence term (base[1] != base[0], U != 0).
-template <bool EXACT, bool SITE, bool DG>
+template <bool EXACT, bool SITE, bool DG, bool CREG>
 __device__ __forceinline__ void apply4(const T4& T, const StencilConst& K, int r, double2 hp,
                                        double srow, const Row4& up, const Row4& mid,
                                        const Row4& dn, double2 lf, double2 rt, double ci,
                                        Row4& out) {
   const int d = r - kCols * T.p;  // diagonal column offset within the thread's four
-  const ColC C = load_colc<SITE>(T);
+  const ColC C = load_colc<SITE, CREG>(T);
 #pragma unroll
   for (int q = 0; q < kCols; ++q) {
     double v0 = (DG && d == q) ? K.base[1] : K.base[0];
@@ -313,7 +325,7 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   const double2 rt = smem4[L::xl(g, K - 2, buf ^ 1) + T.pr];
   const double ci = RK4 ? a.ci[0] : a.ci[K - 1];
   Row4 tk;
-  apply4<EXACT, SITE, DG>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0, R.w[K - 1][sm],
+  apply4<EXACT, SITE, DG, !RK4>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0, R.w[K - 1][sm],
                       R.w[K - 1][s0], R.w[K - 1][sp], lf, rt, ci, tk);
   if constexpr (K == NAPP) {
     const int jo = j - K + 1;
@@ -426,7 +438,7 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
     rt = rmul(P.s, rt);
   }
   Row4 t;
-  apply4<EXACT, SITE, DG>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, psi, dn, lf, rt,
+  apply4<EXACT, SITE, DG, !RK4>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, psi, dn, lf, rt,
                       a.ci[0], t);
   if constexpr (NAPP == 1) {
     Row4 o;
@@ -547,6 +559,9 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
         if (SITE) cc[(kCols + 1 + q) * NP + p] = sg[kCols * p + q];
       }
       cc[kCols * NP + p] = hop[g.wrap(kCols * p - 1)];
+#pragma unroll
+      for (int q = 0; q < kCols; ++q) T.hc[q] = hop[kCols * p + q];
+      T.hm0 = hop[g.wrap(kCols * p - 1)];
     }
     P.s = a.scl ? a.scl[r] : 1.0;
     P.scale = P.s != 1.0;
