@@ -255,11 +255,13 @@ __device__ __forceinline__ Row4 ring_row(const Geo4<NN>& g, const T4& T, int slo
 // (H z)(r, x) for the thread's four columns of row r: up = row r-1,
 // mid = row r, dn = row r+1, lf / rt = columns 4p-1 / 4p+4 of row r.
 // DG: the diagonal carries the coincidence term (base[1] != base[0], U != 0).
-template <bool EXACT, bool SITE, bool DG, bool CREG>
+// HORN: out = psi + i*ci*(H z) (one DFMA per component, the Horner form of
+// the Taylor sum); otherwise out = i*ci*(H z).
+template <bool EXACT, bool SITE, bool DG, bool CREG, bool HORN = false>
 __device__ __forceinline__ void apply4(const T4& T, const StencilConst& K, int r, double2 hp,
                                        double srow, const Row4& up, const Row4& mid,
                                        const Row4& dn, double2 lf, double2 rt, double ci,
-                                       Row4& out) {
+                                       Row4& out, const Row4* psi = nullptr) {
   const int d = r - kCols * T.p;  // diagonal column offset within the thread's four
   const ColC C = load_colc<SITE, CREG>(T);
 #pragma unroll
@@ -274,14 +276,28 @@ __device__ __forceinline__ void apply4(const T4& T, const StencilConst& K, int r
     h = madd<EXACT>(h, hp.x, up.c[q]);  // particle 0 -move: row r-1, hop[r-1]
     h = madd<EXACT>(h, C.hc[q], rr);    // particle 1 +move
     h = madd<EXACT>(h, hm, l);          // particle 1 -move
-    out.c[q] = times_i(ci, h);
+    if constexpr (HORN)
+      out.c[q] = cmake(fma(-ci, h.y, psi->c[q].x), fma(ci, h.x, psi->c[q].y));
+    else
+      out.c[q] = times_i(ci, h);
   }
+}
+
+// FMA-mode Taylor (order >= 2) runs in Horner form,
+//   psi' = psi + c1 H (psi + c2 H (psi + ... (psi + cn H psi))),  ck = -i dt/(hbar k),
+// the same polynomial as the reference's term recursion: stage k applies
+// c_{n-k+1}, adds psi of its row, and the running sums are replaced by a
+// three-row window of psi (Regs4::acc).  12 FP64 instructions per element
+// and application instead of 14.  EXACT keeps the reference's order.
+template <int NAPP, bool RK4, bool EXACT>
+constexpr bool horner4() {
+  return !EXACT && !RK4 && NAPP >= 2;
 }
 
 template <int NAPP>
 struct Regs4 {
   Row4 w[NAPP][3];  // w[k], k >= 1: stage-k output window (input of stage k+1); w[0] unused
-  Row4 acc[3];      // running sums, slot = row mod 3 (relative)
+  Row4 acc[3];      // running sums (Horner: psi), slot = row mod 3 (relative)
   Row4 up;          // psi(j-1): read by stage 1, reused by RK4 stage 2
   double nrm;
 };
@@ -323,17 +339,22 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   const int rr = g.wrap(j - K + 1);
   const double2 lf = smem4[L::xr(g, K - 2, buf ^ 1) + T.pl];
   const double2 rt = smem4[L::xl(g, K - 2, buf ^ 1) + T.pr];
-  const double ci = RK4 ? a.ci[0] : a.ci[K - 1];
+  constexpr bool HORN = horner4<NAPP, RK4, EXACT>();
+  const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[NAPP - K] : a.ci[K - 1]);
   Row4 tk;
-  apply4<EXACT, SITE, DG, !RK4>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0, R.w[K - 1][sm],
-                      R.w[K - 1][s0], R.w[K - 1][sp], lf, rt, ci, tk);
+  apply4<EXACT, SITE, DG, !RK4, HORN>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0,
+                                      R.w[K - 1][sm], R.w[K - 1][s0], R.w[K - 1][sp], lf, rt, ci, tk, &R.acc[s0]);
   if constexpr (K == NAPP) {
     const int jo = j - K + 1;
     Row4 o;
 #pragma unroll
     for (int q = 0; q < kCols; ++q)
-      o.c[q] = RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]);
+      o.c[q] = HORN ? tk.c[q] : (RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]));
     if (jo >= P.ya && jo < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, rr, o, R.nrm);
+  } else if constexpr (HORN) {
+    R.w[K][s0] = tk;
+    smem4[L::xl(g, K - 1, buf) + T.p] = tk.c[0];
+    smem4[L::xr(g, K - 1, buf) + T.p] = tk.c[kCols - 1];
   } else {
     Row4 nk;
     if (RK4) {
@@ -437,9 +458,10 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
     lf = rmul(P.s, lf);
     rt = rmul(P.s, rt);
   }
+  constexpr bool HORN = horner4<NAPP, RK4, EXACT>();
   Row4 t;
-  apply4<EXACT, SITE, DG, !RK4>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, psi, dn, lf, rt,
-                      a.ci[0], t);
+  apply4<EXACT, SITE, DG, !RK4, HORN>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, psi, dn,
+                                      lf, rt, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
   if constexpr (NAPP == 1) {
     Row4 o;
 #pragma unroll
@@ -459,6 +481,11 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
 #pragma unroll
         for (int q = 0; q < kCols; ++q) st[q * g.np() + T.p] = t.c[q];
       }
+    } else if constexpr (HORN) {
+      // psi(j-1) joins the window for stages 2..n (rows j-1 .. j-n+1); its
+      // slot held psi(j-4), which the last stage used one iteration ago
+      R.acc[SM1] = R.up;
+      nt = t;
     } else {
       // acc(j-1) = psi(j-1) + t1(j-1): both are at hand (psi(j-1) was just
       // read, t1(j-1) is window 1), and stage 2 below is its first update.
