@@ -229,9 +229,12 @@ __device__ __forceinline__ void xch_put(const T3& T, int k, int buf, const Quad&
 }
 
 // (H z) on the block at plane r: up / mid / dn = planes r-1, r, r+1.
-template <bool EXACT, bool SITE>
+// out = i*ci*(H z), or with HORN psi + i*ci*(H z) (Horner-form Taylor, as
+// step_band4.cu).
+template <bool EXACT, bool SITE, bool HORN = false>
 __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
-                                       const Quad& dn, const Nb& nb, double ci, Quad& out) {
+                                       const Quad& dn, const Nb& nb, double ci, Quad& out,
+                                       const Quad* psi = nullptr) {
   // couplings re-read from the shared table (hop2[y] = (hop[y-1], hop[y]))
   // at every application: holding them in registers spills
   const double2 h0 = smem3[kHopOff + r];
@@ -263,7 +266,10 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
     h = madd<EXACT>(h, h1[a], x1m);         // particle 1 -move, hop[x1-1]
     h = madd<EXACT>(h, h2[1 + b], x2p);     // particle 2 +move, hop[x2]
     h = madd<EXACT>(h, h2[b], x2m);         // particle 2 -move, hop[x2-1]
-    out.c[q] = times_i(ci, h);
+    if constexpr (HORN)
+      out.c[q] = cmake(fma(-ci, h.y, psi->c[q].x), fma(ci, h.x, psi->c[q].y));
+    else
+      out.c[q] = times_i(ci, h);
   }
 }
 
@@ -367,17 +373,21 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
   constexpr int s0 = ((PH - K + 1) % 3 + 3) % 3;  // acc slot of plane j-K+1
   const int buf = i & 1;
   const int rr = wrap3(j - K + 1);
-  const double ci = RK4 ? a.ci[0] : a.ci[K - 1];
+  constexpr bool HORN = !RK4 && !EXACT;
+  const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[NAPP - K] : a.ci[K - 1]);
   Quad tk;
-  apply3<EXACT, SITE>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk);
+  apply3<EXACT, SITE, HORN>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk, &R.acc[s0]);
   R.old[K - 1] = mid;
   Quad nk;
   if constexpr (K == NAPP) {
     const int jo = j - K + 1;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      nk.c[q] = RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]);
+      nk.c[q] = HORN ? tk.c[q] : (RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]));
     if (jo >= P.ya && jo < P.yb) store3(T, P, rr, nk, R.nrm);
+  } else if constexpr (HORN) {
+    nk = tk;
+    xch_put(T, K - 1, buf, nk);
   } else {
     if (RK4) {
       const Quad pm = ring_quad<SC>(T, (i + (K == 2 ? 0 : kRing3 - 1)) % kRing3, P.s);  // psi(j-1) / psi(j-2)
@@ -419,11 +429,15 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   const Quad psi = ring_quad<SC>(T, sl_mid, P.s);
   const Quad dn = ring_quad<SC>(T, sl_dn, P.s);
   const Nb nb = ring_nb<SC>(T, sl_mid, P.s);
+  constexpr bool HORN = !RK4 && !EXACT;
   Quad t;
-  apply3<EXACT, SITE>(T, a.k, r, R.up, psi, dn, nb, a.ci[0], t);
+  apply3<EXACT, SITE, HORN>(T, a.k, r, R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
   const Quad mid1 = xch_own(T, 0, buf ^ 1);  // t1 (arg1) of plane j-1
   Quad nt;
-  if (RK4) {
+  if (HORN) {
+    R.acc[SM1] = R.up;  // psi(j-1) joins the window for stages 2..4
+    nt = t;
+  } else if (RK4) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) nt.c[q] = cadd(rmul(0.5, t.c[q]), psi.c[q]);
 #pragma unroll

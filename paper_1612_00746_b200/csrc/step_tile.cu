@@ -254,6 +254,9 @@ __global__ void __launch_bounds__(512, 1) resident_kernel(ResArgs a) {
   const double hx = active ? hv[x] : 0.0, hxl = active ? hv[xl] : 0.0;
   const double sxv = (SITE && active) ? sv[x] : 0.0;
   const int applications = RK4 ? 4 : a.order;
+  // FMA-mode Taylor in Horner form (see step_band4.cu): application k applies
+  // c_{order-k} and adds psi (held in acc through the step)
+  constexpr bool HORN = !RK4 && !EXACT;
   RealStat* st_r = a.stats + r;
   EventRec* ev_r = a.events + r * kMaxEvents;
 
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(512, 1) resident_kernel(ResArgs a) {
   for (long long step = 0; step < a.n_steps; ++step) {
 #pragma unroll 1
     for (int k = 0; k < applications; ++k) {
-      const double ci = RK4 ? a.ci[0] : a.ci[k];
+      const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[applications - 1 - k] : a.ci[k]);
       if (active) {
         double2 prev = tile[(y0 == 0 ? n - 1 : y0 - 1) * n + x];
 #pragma unroll
@@ -281,6 +284,10 @@ __global__ void __launch_bounds__(512, 1) resident_kernel(ResArgs a) {
             h = madd<EXACT>(h, hx, rt);
             h = madd<EXACT>(h, hxl, lf);
             prev = cur[i];
+            if (HORN) {
+              cur[i] = cmake(fma(-ci, h.y, acc[i].x), fma(ci, h.x, acc[i].y));
+              continue;
+            }
             const double2 stg = times_i(ci, h);
             if (!RK4) {
               cur[i] = stg;
@@ -310,6 +317,10 @@ __global__ void __launch_bounds__(512, 1) resident_kernel(ResArgs a) {
           if (y0 + i < n) tile[(y0 + i) * n + x] = cur[i];
       }
       __syncthreads();
+    }
+    if (HORN && active) {
+#pragma unroll
+      for (int i = 0; i < kSR; ++i) acc[i] = cur[i];
     }
     // norm policy for this step
     double nrm = 0.0;
