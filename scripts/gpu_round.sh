@@ -2,7 +2,7 @@
 # Full GPU evidence pass (run under gpurun): tests, smoke, bench (both arms),
 # sweep, ncu launch list of the default bench, ncu --set full of each kernel.
 set -u
-TAG=${1:-r01b}
+TAG=${1:-r01c}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
@@ -21,5 +21,7 @@ for spec in "band4_n256_fma|band4|" "band4_n256_exact|band4|--exact" "band4_n102
     -o $OUT/$name python bench.py --no-e2e --no-cpu --steps 4 --warmup 3 $args > $OUT/$name.log 2>&1
   ncu -i $OUT/$name.ncu-rep --page details --csv > $OUT/${name}_details.csv 2>/dev/null
   ncu -i $OUT/$name.ncu-rep --page raw --csv > $OUT/${name}_raw.csv 2>/dev/null
+  ncu -i $OUT/$name.ncu-rep --page source --csv --print-source sass > $OUT/${name}_sass.csv 2>/dev/null
+  rm -f $OUT/$name.ncu-rep  # reports exceed the copy-back limit; the CSV exports stay
 done
 tail -3 $OUT/pytest_gpu.log; tail -2 $OUT/smoke.log; cat $OUT/bench.json $OUT/bench_ref.json $OUT/sweep.jsonl
