@@ -272,10 +272,21 @@ __device__ __forceinline__ void apply4(const T4& T, const StencilConst& K, int r
     const double2 rr = q == kCols - 1 ? rt : mid.c[q + 1];
     const double hm = q == 0 ? C.hm0 : C.hc[q - 1];
     double2 h = rmul(v0, mid.c[q]);
-    h = madd<EXACT>(h, hp.y, dn.c[q]);  // particle 0 +move: row r+1, hop[r]
-    h = madd<EXACT>(h, hp.x, up.c[q]);  // particle 0 -move: row r-1, hop[r-1]
-    h = madd<EXACT>(h, C.hc[q], rr);    // particle 1 +move
-    h = madd<EXACT>(h, hm, l);          // particle 1 -move
+    if constexpr (EXACT) {
+      h = madd<EXACT>(h, hp.y, dn.c[q]);  // particle 0 +move: row r+1, hop[r]
+      h = madd<EXACT>(h, hp.x, up.c[q]);  // particle 0 -move: row r-1, hop[r-1]
+      h = madd<EXACT>(h, C.hc[q], rr);    // particle 1 +move
+      h = madd<EXACT>(h, hm, l);          // particle 1 -move
+    } else {
+      // FMA mode: row r+1 last.  In the pipeline it is the only input the
+      // previous stage produced in this same iteration, so everything else
+      // can issue before that stage finishes (two dependent DFMAs per stage
+      // on the critical path instead of six).
+      h = madd<EXACT>(h, hp.x, up.c[q]);
+      h = madd<EXACT>(h, C.hc[q], rr);
+      h = madd<EXACT>(h, hm, l);
+      h = madd<EXACT>(h, hp.y, dn.c[q]);
+    }
     if constexpr (HORN)
       out.c[q] = cmake(fma(-ci, h.y, psi->c[q].x), fma(ci, h.x, psi->c[q].y));
     else

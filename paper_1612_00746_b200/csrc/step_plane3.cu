@@ -260,12 +260,15 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
     const double2 x2p = b == 1 ? nb.x2p[a] : mid.c[2 * a + 1];
     const double2 x2m = b == 0 ? nb.x2m[a] : mid.c[2 * a];
     double2 h = rmul(v0, mid.c[q]);
-    h = madd<EXACT>(h, h0.y, dn.c[q]);        // particle 0 +move (plane r+1), hop[x0]
+    if (EXACT) h = madd<EXACT>(h, h0.y, dn.c[q]);  // particle 0 +move (plane r+1), hop[x0]
     h = madd<EXACT>(h, h0.x, up.c[q]);        // particle 0 -move (plane r-1), hop[x0-1]
     h = madd<EXACT>(h, h1[1 + a], x1p);     // particle 1 +move, hop[x1]
     h = madd<EXACT>(h, h1[a], x1m);         // particle 1 -move, hop[x1-1]
     h = madd<EXACT>(h, h2[1 + b], x2p);     // particle 2 +move, hop[x2]
     h = madd<EXACT>(h, h2[b], x2m);         // particle 2 -move, hop[x2-1]
+    // FMA mode: plane r+1 last, the one input the previous stage produced in
+    // this iteration (as step_band4.cu)
+    if (!EXACT) h = madd<EXACT>(h, h0.y, dn.c[q]);
     if constexpr (HORN)
       out.c[q] = cmake(fma(-ci, h.y, psi->c[q].x), fma(ci, h.x, psi->c[q].y));
     else
