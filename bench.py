@@ -181,17 +181,23 @@ def reference_arm(a):
 
 
 def workload_config(a):
+    state_gib = a.realizations * a.n ** a.m * 16 / 2**30
+    label = "configs[1]: " if (a.m, a.n) == (2, 256) else ""
+    noise = "static tunnelling noise" if a.rate == 0 else f"telegraph tunnelling noise (rate {a.rate})"
     return {
-        "workload": f"configs[1]: m={a.m} particles, N={a.n} ring (D={a.n ** a.m}), "
-                    f"{a.realizations} realizations per GPU, static tunnelling noise, "
+        "workload": f"{label}m={a.m} particles, N={a.n} ring (D={a.n ** a.m}), "
+                    f"{a.realizations} realizations per GPU, {noise}, "
                     f"{a.backend}{'' if a.backend == 'rk4' else '-' + str(a.order)}, dt={a.dt}, "
                     f"norm policy every step, diagonal observables at the last step",
         "n_sites": a.n, "particles": a.m, "realizations_per_gpu": a.realizations,
         "backend": a.backend, "taylor_order": a.order, "dt": a.dt,
         "exact_order": bool(a.exact),
         "arithmetic": ("exact reference order (bit-identical between renormalisations)" if a.exact else
-                       "FMA-contracted stencil, FP64, <= 1e-12 from the reference (tests/test_gpu_parity.py)"),
-        "l2_policy": "inputs larger than L2 (state stack 1 GiB per buffer per GPU)",
+                       "FMA-contracted stencil (Horner-form Taylor), FP64, <= 1e-12 from the reference "
+                       "(tests/test_gpu_parity.py)"),
+        "l2_policy": (f"inputs larger than L2 (state stack {state_gib:.2f} GiB per buffer per GPU, L2 126 MB)"
+                      if state_gib * 2**30 > 126e6 else
+                      f"state stack {state_gib * 1024:.0f} MiB per GPU fits in L2: not an HBM measurement"),
     }
 
 
@@ -305,10 +311,19 @@ def ours(a):
     # the distributed path -- barriers, MAX reductions, run(group=...) -- runs)
     distributed = "RANK" in os.environ and "MASTER_ADDR" in os.environ
     rank = int(os.environ.get("RANK", "0"))
+    # CTQW_DIST_BACKEND=gloo lets several ranks share one GPU, to exercise the
+    # N > 1 code path (barriers, MAX reductions, sharded run()) on a one-GPU
+    # box; measurements use NCCL with one GPU per rank
+    backend = os.environ.get("CTQW_DIST_BACKEND", "nccl")
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if distributed:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     R_total = a.realizations * world
     obs = ("populations", "position_mean_variance", "participation_ratio")
     cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([a.n]), a.m),
