@@ -87,6 +87,12 @@ __device__ __forceinline__ double2 times_i(double ci, double2 z) {
   return cmake(__dmul_rn(-z.y, ci), __dmul_rn(z.x, ci));
 }
 
+// x + (0 + w i) * h with one DFMA per component (FMA-mode stage arithmetic:
+// the Taylor/RK4 coefficient times i folded into the accumulation)
+__device__ __forceinline__ double2 ifma(double2 x, double w, double2 h) {
+  return cmake(fma(-w, h.y, x.x), fma(w, h.x, x.y));
+}
+
 __device__ __forceinline__ double norm2(double2 z) { return z.x * z.x + z.y * z.y; }
 
 __device__ __forceinline__ int wrap(int x, int n) {
