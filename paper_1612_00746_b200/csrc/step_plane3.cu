@@ -62,6 +62,7 @@ struct Plane3Args {
   Coef coef;
   StencilConst k;
   double ci[4];
+  double rkw[4];     // FMA-mode RK4 weights times c: c/2, c/3, c/6 (constant bank operands)
   const double* scl;
   double* partial;
   const long long* fail;
@@ -231,7 +232,7 @@ __device__ __forceinline__ void xch_put(const T3& T, int k, int buf, const Quad&
 // (H z) on the block at plane r: up / mid / dn = planes r-1, r, r+1.
 // out = i*ci*(H z), or with HORN psi + i*ci*(H z) (Horner-form Taylor, as
 // step_band4.cu).
-template <bool EXACT, bool SITE, bool HORN = false>
+template <bool EXACT, bool SITE, bool HORN = false, bool RAW = false>
 __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
                                        const Quad& dn, const Nb& nb, double ci, Quad& out,
                                        const Quad* psi = nullptr) {
@@ -270,7 +271,9 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
     // this iteration (as step_band4.cu)
     if (!EXACT) h = madd<EXACT>(h, h0.y, dn.c[q]);
     if constexpr (HORN)
-      out.c[q] = cmake(fma(-ci, h.y, psi->c[q].x), fma(ci, h.x, psi->c[q].y));
+      out.c[q] = ifma(psi->c[q], ci, h);
+    else if constexpr (RAW)
+      out.c[q] = h;  // FMA-mode RK4: the caller folds i*c into its combinations
     else
       out.c[q] = times_i(ci, h);
   }
@@ -377,11 +380,31 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
   const int buf = i & 1;
   const int rr = wrap3(j - K + 1);
   constexpr bool HORN = !RK4 && !EXACT;
+  // as step_band4.cu: one DFMA per stage combination (not with on-site noise,
+  // whose extra table reads would spill)
+  constexpr bool RKF = RK4 && !EXACT && !SITE;
   const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[NAPP - K] : a.ci[K - 1]);
   Quad tk;
-  apply3<EXACT, SITE, HORN>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk, &R.acc[s0]);
+  apply3<EXACT, SITE, HORN, RKF>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk, &R.acc[s0]);
   R.old[K - 1] = mid;
   Quad nk;
+  if constexpr (RKF) {
+    if constexpr (K == NAPP) {
+      const int jo = j - K + 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nk.c[q] = ifma(R.acc[s0].c[q], a.rkw[2], tk.c[q]);
+      if (jo >= P.ya && jo < P.yb) store3(T, P, rr, nk, R.nrm);
+    } else {
+      const Quad pm = ring_quad<SC>(T, (i + (K == 2 ? 0 : kRing3 - 1)) % kRing3, P.s);  // psi(j-1) / psi(j-2)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        nk.c[q] = ifma(pm.c[q], K == 2 ? a.rkw[0] : ci, tk.c[q]);
+        R.acc[s0].c[q] = ifma(R.acc[s0].c[q], a.rkw[1], tk.c[q]);
+      }
+      xch_put(T, K - 1, buf, nk);
+    }
+    return nk;
+  }
   if constexpr (K == NAPP) {
     const int jo = j - K + 1;
 #pragma unroll
@@ -433,11 +456,19 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   const Quad dn = ring_quad<SC>(T, sl_dn, P.s);
   const Nb nb = ring_nb<SC>(T, sl_mid, P.s);
   constexpr bool HORN = !RK4 && !EXACT;
+  constexpr bool RKF = RK4 && !EXACT && !SITE;
   Quad t;
-  apply3<EXACT, SITE, HORN>(T, a.k, r, R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
+  apply3<EXACT, SITE, HORN, RKF>(T, a.k, r, R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
   const Quad mid1 = xch_own(T, 0, buf ^ 1);  // t1 (arg1) of plane j-1
   Quad nt;
-  if (HORN) {
+  if constexpr (RKF) {
+    // t = H psi: arg = psi + k1/2; acc(j) = psi + k1/6 waits in t
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      nt.c[q] = ifma(psi.c[q], a.rkw[0], t.c[q]);
+      t.c[q] = ifma(psi.c[q], a.rkw[2], t.c[q]);
+    }
+  } else if (HORN) {
     R.acc[SM1] = R.up;  // psi(j-1) joins the window for stages 2..4
     nt = t;
   } else if (RK4) {
@@ -706,6 +737,10 @@ cudaError_t launch_plane3_step(const double2* psi_in, double2* psi_out, int64_t 
   a.coef = coef;
   a.k = k;
   for (int i = 0; i < 4; ++i) a.ci[i] = sc.ci[i];
+  a.rkw[0] = 0.5 * sc.ci[0];
+  a.rkw[1] = sc.ci[0] * (1.0 / 3.0);
+  a.rkw[2] = sc.ci[0] * (1.0 / 6.0);
+  a.rkw[3] = 0.0;
   a.scl = scl;
   a.partial = partial;
   a.fail = fail;
