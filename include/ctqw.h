@@ -64,14 +64,15 @@ typedef struct {
 /* Integrator + norm policy.  Mirrors StepperConfig (propagators.py:61-86). */
 typedef struct {
   int32_t backend;     /* CTQW_BACKEND_TAYLOR / CTQW_BACKEND_RK4 */
-  int32_t order;       /* Taylor order (ignored for RK4) */
+  int32_t order;       /* Taylor order, 1..64 (ignored for RK4) */
   double dt;
   double tol_norm;
   double tol_fail;
   int32_t renormalize;
   int32_t exact;       /* 1: reference operation order, no FMA contraction
                           (bit-identical to the reference between rescales);
-                          0: FMA-contracted stencil (<= 1e-14 from it) */
+                          0: FMA-contracted stencil, Horner-form Taylor
+                          (<= 1e-12 from it) */
 } ctqw_stepper_t;
 
 /* NormEvent (propagators.py:89-96). */

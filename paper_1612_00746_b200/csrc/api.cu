@@ -188,8 +188,8 @@ int validate_stepper(ctqw_ctx* h, const ctqw_stepper_t* st) {
     return fail_with(h, CTQW_ERR_CONFIG, "backend must be taylor or rk4 (eigen is not on the B200 path)");
   if (!(std::isfinite(st->dt) && st->dt > 0))
     return fail_with(h, CTQW_ERR_CONFIG, "dt must be positive and finite");
-  if (st->backend == CTQW_BACKEND_TAYLOR && (st->order < 1 || st->order > 16))
-    return fail_with(h, CTQW_ERR_CONFIG, "taylor_order must be in [1, 16] on the B200 path");
+  if (st->backend == CTQW_BACKEND_TAYLOR && (st->order < 1 || st->order > kMaxTaylorOrder))
+    return fail_with(h, CTQW_ERR_CONFIG, "taylor_order must be in [1, 64] on the B200 path");
   if (!(0 < st->tol_norm && st->tol_norm < st->tol_fail))
     return fail_with(h, CTQW_ERR_CONFIG, "need 0 < tol_norm < tol_fail");
   return CTQW_OK;

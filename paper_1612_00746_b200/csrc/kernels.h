@@ -36,10 +36,12 @@ struct StencilConst {
 
 // Taylor / RK4 scalars, computed on the host exactly as the reference does
 // (coeff = -1j*dt/hbar, coeff/j; propagators.py:185,191).
+constexpr int kMaxTaylorOrder = 64;
+
 struct StepScalars {
   int backend;  // 0 taylor, 1 rk4
   int order;    // Taylor order (applications per step); 4 for RK4
-  double ci[16];  // imaginary part of coeff/j, j = 1..order (taylor); ci[0] = coeff (rk4)
+  double ci[kMaxTaylorOrder];  // imaginary part of coeff/j, j = 1..order (taylor); ci[0] = coeff (rk4)
 };
 
 int generic_parts(int64_t dim);

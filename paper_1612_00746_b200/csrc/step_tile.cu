@@ -199,7 +199,7 @@ struct ResArgs {
   Coef coef;
   StencilConst k;
   int order;
-  double ci[16];
+  double ci[kMaxTaylorOrder];
   NormPolicy pol;
   long long first_step;
   long long n_steps;
@@ -461,7 +461,7 @@ cudaError_t launch_resident(double2* psi, int64_t count, int n, const Coef& coef
   a.coef = coef;
   a.k = k;
   a.order = sc.order;
-  for (int i = 0; i < 16; ++i) a.ci[i] = sc.ci[i];
+  for (int i = 0; i < kMaxTaylorOrder; ++i) a.ci[i] = sc.ci[i];
   a.pol = pol;
   a.first_step = first_step;
   a.n_steps = n_steps;
