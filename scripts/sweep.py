@@ -22,6 +22,7 @@ try:
         PEAK = float(json.load(_f)["hbm_gbs"]) * 1e9
 except Exception:
     PEAK = 6544e9
+ONLY = ""
 
 
 def timed(ens, cfg, steps, post_rate, engine, torch):
@@ -45,6 +46,8 @@ def timed(ens, cfg, steps, post_rate, engine, torch):
 
 def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling", post_rates=(None,), rate=0.0,
              observables=("populations", "position_mean_variance", "participation_ratio")):
+    if ONLY and ONLY not in name:
+        return
     import torch
 
     import paper_1612_00746_b200 as p
@@ -81,8 +84,11 @@ def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling"
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="", help="run only the cases whose name contains this")
     a = ap.parse_args()
     q = a.quick
+    global ONLY
+    ONLY = a.only
     # configs[0]: N=64, 100 realizations (resident kernel), Taylor, post every 10 steps
     run_case("configs[0] N=64 R=100", 2, 64, 100, 300 if q else 1500, post_rates=(10, None),
              observables=("populations", "position_mean_variance", "purity", "participation_ratio"))
