@@ -9,14 +9,19 @@
 // computes plane j-k+1 from the three-plane register window of stage k-1's
 // output (own amplitudes) plus the in-plane neighbours of plane j-k+1 that
 // stage k-1 published one iteration earlier.  In-plane neighbours along x2
-// and inside the band along x1 come from the CTA's shared memory; the two x1
-// rows across the band edges come from the neighbouring CTAs' shared memory
-// (DSMEM).  One cluster barrier per plane replaces __syncthreads.
+// and inside the band along x1 come from the CTA's shared memory.  The two
+// x1 rows across the band edges are pushed by the neighbouring CTAs straight
+// into this CTA's halo rows with st.async (DSMEM), each push counted on this
+// CTA's "full" mbarrier, so the data needs no fence to be visible.  Per
+// plane: one CTA barrier (own exchange rows) and one relaxed cluster barrier
+// (every CTA has consumed the halo rows the next pushes overwrite); the
+// release form of the cluster arrive would cost a GPU-scope fence per plane
+// (MEMBAR.ALL.GPU + ERRBAR, ~15 % of the time, profiles/r01c).
 //
 // Threads: 256 per CTA, thread (u, v) owns the 2x2 block x1 = 8c + 2u + {0,1},
 // x2 = 2v + {0,1}.  psi planes arrive by TMA (ten 2 KB rows per plane: the
 // band plus one halo row on each side, so stage 1 needs no DSMEM), 128B
-// swizzled, into a 6-plane ring with one mbarrier per slot.
+// swizzled, into a 5-plane ring with one mbarrier per slot.
 //
 // Arithmetic is the reference's (hamiltonian.py:205-222): diagonal
 // base[#coincident pairs] + ((site[x0] + site[x1]) + site[x2]), then for each
@@ -44,8 +49,7 @@ constexpr int kN3 = 128;             // lattice sites
 constexpr int kCl = 16;              // CTAs per cluster (x1 bands)
 constexpr int kBand = kN3 / kCl;     // x1 rows per CTA
 constexpr int kTR = kBand + 2;       // ring rows per plane (band + x1 halo)
-constexpr int kRing3 = 6;            // psi planes resident
-constexpr int kPref3 = 3;            // planes requested ahead of the one consumed
+constexpr int kRing3 = 5;            // psi planes resident
 constexpr int kThreads3 = 256;       // 4 x1 pairs x 64 x2 pairs
 constexpr int kPB = 16;              // planes per norm block
 constexpr int kNblk3 = kN3 / kPB;    // norm blocks per realization per CTA
@@ -96,19 +100,33 @@ struct Quad {
   double2 c[4];
 };
 
+// planes requested ahead of the one consumed: the ring holds psi(j-1 .. j+1)
+// at iteration j, RK4 also psi(j-2), and one slot is being refilled
+template <bool RK4>
+constexpr int pref3() {
+  return RK4 ? kRing3 - 3 : kRing3 - 2;
+}
+
 // Shared memory (byte offsets from smem3): ring [kRing3][kTR][128] chunks;
 // exchange [3 stages][2 parity][kBand][128] chunks; hop2 [N] (hop[y-1],
-// hop[y]); site [N]; red [8] per-warp norm partials; mbarriers [kRing3].
+// hop[y]); site [N]; red [8] per-warp norm partials; mbarriers [kRing3 + 6].
+// After the exchange: halo [3 stages][2 parity][2 sides][128] chunks, the x1
+// rows across the band edges, pushed there by the neighbouring CTAs.
 extern __shared__ __align__(1024) double2 smem3[];
 constexpr int kXOff = kRing3 * kTR * kN3;        // exchange, in double2 units
 constexpr int kXStage = 2 * kBand * kN3;
-constexpr int kHopOff = kXOff + 3 * kXStage;
+constexpr int kHaloOff = kXOff + 3 * kXStage;
+constexpr int kHopOff = kHaloOff + 3 * 2 * 2 * kN3;
 constexpr int kSiteOff = kHopOff + kN3;          // doubles follow, in double2 units of the base
-constexpr size_t kSmem3 = (size_t)(kSiteOff) * 16 + (size_t)kN3 * 8 + 16 * 8 + kRing3 * 8;
+constexpr int kBars3 = kRing3 + 6;               // ring slots, halo "full" [3 stages][2 parity]
+constexpr size_t kSmem3 = (size_t)(kSiteOff) * 16 + (size_t)kN3 * 8 + 16 * 8 + kBars3 * 8;
 
 __device__ __forceinline__ double* site_tab() { return reinterpret_cast<double*>(smem3 + kSiteOff); }
 __device__ __forceinline__ double* red_tab() { return site_tab() + kN3; }
 __device__ __forceinline__ uint32_t bar_addr(int slot) { return s_u32(red_tab() + 16) + 8 * slot; }
+// halo k (stage output index) of parity p has landed: armed locally with the
+// expected bytes, completed by the neighbours' st.async pushes
+__device__ __forceinline__ uint32_t full_bar(int k, int p) { return bar_addr(kRing3 + 2 * k + p); }
 
 struct T3 {
   int u, v, c;          // x1 pair, x2 pair, cluster rank (x1 band)
@@ -119,11 +137,17 @@ struct T3 {
   uint32_t dn_nb;       // ... in rank c+1 (x1 row below the band)
 };
 
-__device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
-  double2 v;
-  // volatile: stays ordered after the cluster wait (asm volatile, memory clobber)
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-  return v;
+__device__ __forceinline__ void mbar_arm3(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+// Push 16 bytes into a neighbour's shared memory; the bytes count toward the
+// transaction of its mbarrier, so the data needs no fence to be seen there.
+__device__ __forceinline__ void st_async16(uint32_t cluster_addr, double2 v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                   cluster_addr),
+               "d"(v.x), "d"(v.y), "r"(cluster_bar)
+               : "memory");
 }
 
 struct Piece3 {
@@ -135,6 +159,7 @@ struct Piece3 {
   double s;
   bool scale;
   int pend, pend2;
+  int iters;  // iterations the loop executes (phase-unrolled by 3); the last pushes nothing
   uint32_t* ph;
 };
 
@@ -200,6 +225,12 @@ __device__ __forceinline__ int xoff(int k, int buf, int row, int col) {
   return kXOff + k * kXStage + (buf * kBand + row) * kN3 + (col & 1) * (kN3 / 2) + (col >> 1);
 }
 
+// halo element: stage k, parity p, side d (0: the x1 row above the band, 1:
+// below), x2 column; even columns first as in the exchange rows
+__device__ __forceinline__ int hoff(int k, int p, int d, int col) {
+  return kHaloOff + ((k * 2 + p) * 2 + d) * kN3 + (col & 1) * (kN3 / 2) + (col >> 1);
+}
+
 __device__ __forceinline__ Nb xch_nb(const T3& T, int k, int buf) {
   Nb nb;
 #pragma unroll
@@ -207,14 +238,33 @@ __device__ __forceinline__ Nb xch_nb(const T3& T, int k, int buf) {
     nb.x2m[t] = smem3[xoff(k, buf, 2 * T.u + t, wrap3(2 * T.v - 1))];
     nb.x2p[t] = smem3[xoff(k, buf, 2 * T.u + t, wrap3(2 * T.v + 2))];
     const int cm = 2 * T.v + t;
-    // rows across the band edge live in the neighbouring CTA (DSMEM);
-    // u is warp-uniform, so these branches do not diverge
-    if (T.u > 0) nb.x1m[t] = smem3[xoff(k, buf, 2 * T.u - 1, cm)];
-    else nb.x1m[t] = ld_dsmem(T.up_nb + 16u * (uint32_t)xoff(k, buf, kBand - 1, cm));
-    if (T.u < 3) nb.x1p[t] = smem3[xoff(k, buf, 2 * T.u + 2, cm)];
-    else nb.x1p[t] = ld_dsmem(T.dn_nb + 16u * (uint32_t)xoff(k, buf, 0, cm));
+    // rows across the band edges were pushed into the halo rows by the
+    // neighbouring CTAs; u is warp-uniform, so these branches do not diverge
+    nb.x1m[t] = T.u > 0 ? smem3[xoff(k, buf, 2 * T.u - 1, cm)] : smem3[hoff(k, buf, 0, cm)];
+    nb.x1p[t] = T.u < 3 ? smem3[xoff(k, buf, 2 * T.u + 2, cm)] : smem3[hoff(k, buf, 1, cm)];
   }
   return nb;
+}
+
+// Push the band's edge rows of stage k's output (parity p) to the
+// neighbours: u == 0 holds band row 0, the row below rank c-1's band; u == 3
+// holds row kBand-1, the row above rank c+1's.
+__device__ __forceinline__ void halo_push(const T3& T, int k, int p, const Quad& v) {
+  if (T.u == 0) {
+    const uint32_t bar = T.up_nb + (full_bar(k, p) - s_u32(smem3));
+#pragma unroll
+    for (int t = 0; t < 2; ++t) st_async16(T.up_nb + 16u * (uint32_t)hoff(k, p, 1, 2 * T.v + t), v.c[t], bar);
+  } else if (T.u == 3) {
+    const uint32_t bar = T.dn_nb + (full_bar(k, p) - s_u32(smem3));
+#pragma unroll
+    for (int t = 0; t < 2; ++t) st_async16(T.dn_nb + 16u * (uint32_t)hoff(k, p, 0, 2 * T.v + t), v.c[2 + t], bar);
+  }
+}
+
+// Before stage k+2 of iteration i reads the halo rows of stage k's output of
+// iteration i-1: the edge warps wait for the neighbours' pushes.
+__device__ __forceinline__ void halo_wait(const T3& T, int k, int i) {
+  if (i >= 1 && (T.u == 0 || T.u == 3)) mbar_wait3(full_bar(k, (i - 1) & 1), ((i - 1) >> 1) & 1);
 }
 
 __device__ __forceinline__ Quad xch_own(const T3& T, int k, int buf) {
@@ -358,8 +408,15 @@ __device__ __forceinline__ void wait_plane(Piece3& P, int rho) {
   }
 }
 
+// End of an iteration.  The CTA barrier orders this CTA's exchange rows for
+// its own warps; the halo rows reach the neighbours through st.async and
+// their mbarriers, so the cluster barrier only has to say "every read of the
+// halo rows pushed one iteration ago has retired" (all of them were consumed
+// by this iteration's arithmetic before the arrive): a relaxed arrive, with
+// no GPU-scope fence.
 __device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -402,6 +459,7 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
         R.acc[s0].c[q] = ifma(R.acc[s0].c[q], a.rkw[1], tk.c[q]);
       }
       xch_put(T, K - 1, buf, nk);
+      if (i < P.iters - 1) halo_push(T, K - 1, buf, nk);
     }
     return nk;
   }
@@ -414,6 +472,7 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
   } else if constexpr (HORN) {
     nk = tk;
     xch_put(T, K - 1, buf, nk);
+    if (i < P.iters - 1) halo_push(T, K - 1, buf, nk);
   } else {
     if (RK4) {
       const Quad pm = ring_quad<SC>(T, (i + (K == 2 ? 0 : kRing3 - 1)) % kRing3, P.s);  // psi(j-1) / psi(j-2)
@@ -427,6 +486,7 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
       for (int q = 0; q < 4; ++q) R.acc[s0].c[q] = cadd(R.acc[s0].c[q], tk.c[q]);
     }
     xch_put(T, K - 1, buf, nk);
+    if (i < P.iters - 1) halo_push(T, K - 1, buf, nk);
   }
   return nk;
 }
@@ -435,18 +495,24 @@ template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH>
 __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i) {
   const int j = P.j0 + i;
   wait_plane(P, i + 2);
-  // the neighbours' exchange planes of the last iteration (own CTA's: the
-  // __syncthreads before the last signal)
-  // pairs with the arrive after stage 3 of the last iteration: its exchange
-  // planes are visible cluster-wide and its ring / exchange reads retired
+  // pairs with the arrives at the end of the last iteration: every CTA of
+  // the cluster has consumed the halo rows this iteration overwrites, and
+  // (through the CTA barrier inside the arrive) this CTA's exchange rows and
+  // ring reads of the last iteration are published / retired
   if (i > 0) cluster_wait();
   // The wait pairs with arrives made before this thread's (and every other
   // thread's) wait_plane above, so it does not order the rescale writes of
   // wait_plane; a CTA barrier does.  Only pieces with a pending rescale pay it.
   if (i == 0 || P.scale) __syncthreads();
   flush3(T, P);
-  if (i + kPref3 + 1 <= P.last_rho) load_plane(a, T, P, i + kPref3 + 1);
+  if (i + pref3<RK4>() + 1 <= P.last_rho) load_plane(a, T, P, i + pref3<RK4>() + 1);
   const int buf = i & 1;
+  // arm the barriers that count this iteration's incoming halo pushes (their
+  // previous phase, iteration i-2's pushes, was awaited by warp 0 last iteration)
+  if (i < P.iters - 1 && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mbar_arm3(full_bar(k, buf), 2 * kN3 * 16);
+  }
   constexpr double c16 = 1.0 / 6.0;
   constexpr int SM1 = (PH + 2) % 3;
   const int r = wrap3(j);
@@ -483,16 +549,17 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
     nt = t;
   }
   xch_put(T, 0, buf, nt);
+  if (i < P.iters - 1) halo_push(T, 0, buf, nt);
+  halo_wait(T, 0, i);
   const Quad t2 = plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
+  halo_wait(T, 1, i);
   const Quad t3 = plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 3>(a, T, P, R, i, j, xch_own(T, 1, buf ^ 1), t2,
                                                                   xch_nb(T, 1, buf ^ 1));
-  // The last stage publishes nothing: load what it reads from the exchange
-  // buffers, then arrive, so the barrier latency overlaps the last stage.
-  const Nb nb4 = xch_nb(T, NAPP - 2, buf ^ 1);
-  const Quad mid4 = xch_own(T, NAPP - 2, buf ^ 1);
-  cluster_arrive();
-  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, NAPP>(a, T, P, R, i, j, mid4, t3, nb4);
+  halo_wait(T, 2, i);
+  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, NAPP>(a, T, P, R, i, j, xch_own(T, NAPP - 2, buf ^ 1), t3,
+                                                     xch_nb(T, NAPP - 2, buf ^ 1));
   if (RK4) R.acc[PH] = t;
+  cluster_arrive();
 }
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC>
@@ -529,7 +596,7 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
   }
   uint32_t ph_bits = 0;
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kRing3; ++q)
+    for (int q = 0; q < kBars3; ++q)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_addr(q)), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -579,8 +646,9 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     P.ph = &ph_bits;
     P.j0 = P.ya - NAPP + 1;
     const int iters = (P.yb - P.ya) + 2 * (NAPP - 1);
+    P.iters = (iters + 2) / 3 * 3;
     P.last_rho = iters + 1;
-    for (int rho = 0; rho <= kPref3; ++rho)
+    for (int rho = 0; rho <= pref3<RK4>(); ++rho)
       if (rho <= P.last_rho) load_plane(a, T, P, rho);
     wait_plane(P, 0);
     wait_plane(P, 1);
@@ -599,6 +667,15 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     cluster_wait();   // completes the last iteration's arrive
     __syncthreads();  // the last stage has written its norm partials
     flush3(T, P, true);
+    // every halo push of the piece has been awaited: restart the halo
+    // barriers at phase 0 for the next piece (published by its cluster barrier)
+    if (threadIdx.x == 0) {
+      for (int q = kRing3; q < kBars3; ++q) {
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar_addr(q)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_addr(q)), "r"(1) : "memory");
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     if (P.side) {
       // every CTA has read planes 0..kWrap-1 (its band and halo rows) for the
       // last time: move the parked output planes in; each thread copies the
