@@ -432,8 +432,8 @@ def ours(a):
                "h2d_bytes_per_step": h2d / a.steps, "d2h_bytes_per_step": d2h / a.steps,
                "seconds": e2e_s, "api": "paper_1612_00746_b200.run(RunConfig, MemorySinks)"}
 
-    cpu = None
-    if rank == 0 and not a.no_cpu:
+    cpu = None  # the host-core baseline is taken on rank 0 at N = 1 only
+    if rank == 0 and world == 1 and not a.no_cpu:
         cores = host_cores()
         per_core = cpu_sample_size(a.n, a.m)
         rate, cores, wall, steps = cpu_rate(a.n, a.m, a.backend, a.order, a.dt, per_core, a.cpu_seconds, cores)
