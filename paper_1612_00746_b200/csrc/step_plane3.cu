@@ -173,6 +173,7 @@ struct Regs3 {
   Quad old[NAPP];  // old[k]: stage-k output, row (plane) j-k-1 at iteration j; old[0] unused
   Quad acc[3];     // running sums, slot = row mod 3 (relative)
   Quad up;
+  Quad m1;         // stage-1 output of the last iteration (own block), instead of re-reading it
   double nrm;
 };
 
@@ -525,7 +526,7 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   constexpr bool RKF = RK4 && !EXACT && !SITE;
   Quad t;
   apply3<EXACT, SITE, HORN, RKF>(T, a.k, r, R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
-  const Quad mid1 = xch_own(T, 0, buf ^ 1);  // t1 (arg1) of plane j-1
+  const Quad mid1 = R.m1;  // t1 (arg1) of plane j-1
   Quad nt;
   if constexpr (RKF) {
     // t = H psi: arg = psi + k1/2; acc(j) = psi + k1/6 waits in t
@@ -550,6 +551,7 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   }
   xch_put(T, 0, buf, nt);
   if (i < P.iters - 1) halo_push(T, 0, buf, nt);
+  R.m1 = nt;
   halo_wait(T, 0, i);
   const Quad t2 = plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
   halo_wait(T, 1, i);
@@ -658,6 +660,8 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     for (int k = 0; k < NAPP; ++k)
 #pragma unroll
       for (int q = 0; q < 4; ++q) R.old[k].c[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) R.m1.c[q] = make_double2(0.0, 0.0);
 #pragma unroll
     for (int w = 0; w < 3; ++w)
 #pragma unroll
