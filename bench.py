@@ -401,7 +401,7 @@ def ours(a):
         # ncu --set full capture (profiles/), per realization-step, scaled to this launch
         traffic_bytes = traffic["dram_bytes_per_realization_step"] * (hi - lo)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic_bytes,
+                "frac": achieved / peak, "frac_of_spec_8000": achieved / 8000.0, "traffic": traffic_bytes,
                 "traffic_source": traffic.get("source") if traffic_bytes else None,
                 "kernel": kernel,
                 "kernel_ms_avg": avg_launch_ms, "kernel_launches": kernel_launches,
