@@ -232,6 +232,11 @@ int ctqw_kernel_time(ctqw_handle_t h, double *total_ms, int64_t *launches, void 
  * ("band4_kernel", "resident_kernel", ...; "" for the generic path). */
 const char *ctqw_step_kernel(ctqw_handle_t h);
 
+/* Its compile-time specialization, e.g.
+ * "band4_kernel<taylor,napp=4,site=1,exact=0,NN=1024>" (parity tests assert
+ * that the variant a BASELINE configuration runs is the one they check). */
+const char *ctqw_step_variant(ctqw_handle_t h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,7 @@ struct ctqw_ctx {
   long long* tg_sum = nullptr;
   int stream_kind = 0;  // CTQW_STREAM: 0 auto, 1 tile, 2 band, 3 band2, 4 band4, 5 plane3, 6 generic
   const char* stream_kernel = "";  // dominant kernel of the last ctqw_evolve
+  char variant[128] = {0};         // its compile-time specialization (ctqw_step_variant)
   std::string err;
 };
 
@@ -691,6 +692,9 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   // general lattices (move tables) run on the generic kernels only
   if (h->stream_kind == 0 && !h->general && resident_supported(h->m, h->n, sc)) {
     h->stream_kernel = "resident_kernel";
+    std::snprintf(h->variant, sizeof(h->variant), "resident_kernel<%s,order=%d,site=%d,exact=%d,N=%d>",
+                  sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", sc.order, coef.site != nullptr ? 1 : 0,
+                  exact ? 1 : 0, h->n);
     // dynamic noise changes the couplings after every step: one step per launch
     const int64_t chunk = h->tg_enabled ? 1 : n_steps;
     for (int64_t j = 0; j < n_steps; j += chunk) {
@@ -737,6 +741,15 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   if (use_plane3 || use_band4 || use_band2 || use_band || use_tile) {
     h->stream_kernel = use_plane3 ? "plane3_kernel" : use_band4 ? "band4_kernel" : use_band2 ? "band2_kernel"
                        : use_band ? "band_ws_kernel" : "tile_step_kernel";
+    {
+      const int napp = sc.backend == CTQW_BACKEND_RK4 ? 4 : sc.order;
+      // band4 compiles N in for the four-application steps at the BASELINE sizes
+      const int nn = (use_band4 && napp == 4 && (h->n == 256 || h->n == 512 || h->n == 1024)) ? h->n
+                     : use_plane3 ? 128 : 0;
+      std::snprintf(h->variant, sizeof(h->variant), "%s<%s,napp=%d,site=%d,exact=%d,NN=%d>", h->stream_kernel,
+                    sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", napp, coef.site != nullptr ? 1 : 0,
+                    exact ? 1 : 0, nn);
+    }
     const int nparts = use_plane3 ? plane3_parts()
                        : use_band4 ? band4_parts(h->n)
                        : use_band2 ? band2_parts(h->n, sc, coef.site != nullptr, count)
@@ -785,6 +798,8 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   }
   // generic path: in place on psi; work = term buffer A, library scratch B, C
   h->stream_kernel = sc.backend == CTQW_BACKEND_TAYLOR ? "taylor_order_kernel" : "rk4_stage_kernel";
+  std::snprintf(h->variant, sizeof(h->variant), "%s<order=%d,site=%d,exact=%d>", h->stream_kernel, sc.order,
+                coef.site != nullptr ? 1 : 0, exact ? 1 : 0);
   rc = ensure_scratch(h, count * h->dim);
   if (rc) return rc;
   const int nparts = generic_parts(h->dim);
@@ -924,6 +939,7 @@ int ctqw_kernel_timing(ctqw_handle_t h, int32_t enable) {
 }
 
 const char* ctqw_step_kernel(ctqw_handle_t h) { return h ? h->stream_kernel : ""; }
+const char* ctqw_step_variant(ctqw_handle_t h) { return h ? h->variant : ""; }
 
 int ctqw_kernel_time(ctqw_handle_t h, double* total_ms, int64_t* launches, void* stream) {
   if (!h || !total_ms || !launches) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");

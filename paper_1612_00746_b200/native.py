@@ -109,6 +109,7 @@ SIGNATURES = {
     "ctqw_kernel_timing": (ctypes.c_int, [_P, _I32]),
     "ctqw_kernel_time": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
     "ctqw_step_kernel": (ctypes.c_char_p, [_P]),
+    "ctqw_step_variant": (ctypes.c_char_p, [_P]),
     "ctqw_set_lattice": (ctypes.c_int, [_P, _I32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                         ctypes.POINTER(_D)]),
     "ctqw_telegraph_init": (ctypes.c_int, [_P, ctypes.c_uint64, _I64, _I64, ctypes.POINTER(_D), _I32, _I64,
@@ -340,6 +341,10 @@ class Handle:
     def step_kernel(self) -> str:
         """Name of the dominant kernel the last evolve ran ('' = generic path)."""
         return (self.lib.ctqw_step_kernel(self._h) or b"").decode()
+
+    def step_variant(self) -> str:
+        """Its compile-time specialization (template arguments)."""
+        return (self.lib.ctqw_step_variant(self._h) or b"").decode()
 
     def overlap_sumsq(self, a, count_a: int, b, count_b: int, out):
         self._check(self.lib.ctqw_overlap_sumsq(self._h, _ptr(a), int(count_a), _ptr(b),

@@ -327,12 +327,37 @@ def density_fixture():
     np.savez_compressed(os.path.join(HERE, "density.npz"), meta=json.dumps(meta), **arrays)
 
 
+def config0_fixture():
+    """BASELINE configs[0] at full length through the reference's own ``run()``:
+    N=64, m=2, R=100 realizations, static tunnelling noise (+-0.1), Taylor-4,
+    dt=0.02, 1500 steps, post_rate=10 (150 snapshots), default observables
+    (populations, position, purity, participation ratio), dense-rho path."""
+    space = JointSpace(lattice=build_lattice([64]), m=2)
+    cfg = RunConfig(
+        space=space,
+        noise=NoiseSpec(target="tunneling", levels=(-0.1, 0.1), rate=0.0),
+        stepper=StepperConfig(backend="taylor", dt=0.02, taylor_order=4),
+        realizations=100, steps=1500, post_rate=10,
+        master_seed=1234, workers=int(os.environ.get("GOLDEN_WORKERS", "8")), precision="double",
+    )
+    sinks = MemorySinks(keep_densities=False)
+    report = run(cfg, sinks)
+    rows = np.array([r[3] for r in sinks.rows], dtype=np.float64)
+    meta = dict(n=64, m=2, R=100, steps=1500, post_rate=10, backend="taylor", order=4, dt=0.02,
+                target="tunneling", levels=[-0.1, 0.1], master_seed=1234,
+                observables_resolved=list(cfg.observables),
+                rows=[(r[0], r[1], r[2]) for r in sinks.rows],
+                corrections=report.norm_corrections, norm_events=report.norm_events,
+                max_norm_deviation=report.max_norm_deviation, wall_seconds=report.wall_seconds)
+    np.savez_compressed(os.path.join(HERE, "config0_run.npz"), meta=json.dumps(meta), rows=rows)
+
+
 if __name__ == "__main__":
     import sys as _sys
 
     only = _sys.argv[1:]
     for fn in (noise_fixture, stencil_fixture, segment_fixture, run_fixture, telegraph_fixture, density_fixture,
-               lattice_fixture):
+               lattice_fixture, config0_fixture):
         if not only or fn.__name__ in only:
             fn()
     for f in sorted(os.listdir(HERE)):

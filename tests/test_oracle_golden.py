@@ -205,3 +205,21 @@ def test_lattice_run_rows(idx):
     rows = [(t, name, i, v) for t, rr in out for name, i, v in rr]
     assert [(t, nm, i) for t, nm, i, _ in rows] == [tuple(r) for r in c["rows"]]
     np.testing.assert_allclose([v for *_, v in rows], data[f"run{idx}_rows"], rtol=1e-10, atol=1e-13)
+
+
+def test_config0_oracle_prefix_matches_reference_run():
+    """BASELINE configs[0] (N=64, R=100, tunnelling, Taylor-4, dt=0.02, post
+    every 10 steps) through the reference's own run(): the oracle reproduces
+    the first 100 steps (10 snapshots) of the committed 1500-step rows (the
+    full length is checked on the GPU, tests/test_gpu_bench_parity.py)."""
+    data, meta = load_golden("config0_run.npz")
+    n, R, dt = meta["n"], meta["R"], meta["dt"]
+    noise = np.stack([np.random.default_rng((meta["master_seed"], r)).choice(np.array(meta["levels"]), n)
+                      for r in range(R)])
+    st = orc.make_stencil(2, n, 0.0, 1.0, 0.0, link=noise, batch=R)
+    obs = tuple(meta["observables_resolved"])
+    out, _, _ = orc.run_rows(st, orc.product_state(2, n), R, 100, meta["post_rate"], dt, observables=obs)
+    mine = np.array([v for _, rows in out for _, _, v in rows])
+    ref = data["rows"][: mine.size]
+    assert [tuple(r) for r in meta["rows"][: mine.size]] == [(t, nm, i) for t, rows in out for nm, i, _ in rows]
+    np.testing.assert_allclose(mine, ref, rtol=1e-12, atol=1e-14)
