@@ -198,11 +198,25 @@ int ctqw_evolve(ctqw_handle_t h, double *psi_dev, double *work_dev, int64_t coun
  * failed (the stats carry the culprit, as NormFailureError does). */
 int ctqw_segment_stats(ctqw_handle_t h, int64_t r0, ctqw_segment_stats_t *out, void *stream);
 
-/* diag_sum_dev[alpha] (+)= sum_r |psi_r(alpha)|^2, realizations summed in
- * order (the diagonal of accumulate_density's Gram, density.py:91-92,
- * before the division by R).  accumulate = 0 overwrites. */
+/* diag_sum_dev[alpha] (+)= sum_r |psi_r(alpha)|^2 (the diagonal of
+ * accumulate_density's Gram, density.py:91-92, before the division by R).
+ * The sum is exact up to one final rounding and independent of the order of
+ * the realizations (see ctqw_observe_diag_fixed).  accumulate = 0 overwrites. */
 int ctqw_observe_diag(ctqw_handle_t h, const double *psi_dev, int64_t count,
                       double *diag_sum_dev, int32_t accumulate, void *stream);
+
+/* The same sum as exact fixed-point limbs acc_dev[3][N^m] (int64): each
+ * term is split deterministically onto the grids 2^-30, 2^-70, 2^-110 and
+ * added as integers, so the limbs are bitwise independent of realization
+ * order, batching and GPU count; an int64 SUM all-reduce of the limbs across
+ * ranks keeps that (observables identical across 1/2/4/8 GPUs, as the
+ * reference's are across worker counts, pkg/README.md:174-180).  Holds up to
+ * 2^23 realizations.  accumulate = 0 zeroes the limbs first. */
+int ctqw_observe_diag_fixed(ctqw_handle_t h, const double *psi_dev, int64_t count, int64_t *acc_dev,
+                            int32_t accumulate, void *stream);
+/* diag_dev[alpha] = the value of the limbs (carries normalised, then one
+ * rounding per limb pair). */
+int ctqw_fixed_to_double(ctqw_handle_t h, const int64_t *acc_dev, double *diag_dev, void *stream);
 
 /* From the (all-reduced) diagonal sum and the total realization count:
  * populations_dev[N] (observables.py:40-56) and scalars_dev[3] =

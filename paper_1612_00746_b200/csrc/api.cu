@@ -58,6 +58,8 @@ struct ctqw_ctx {
   double* n2_dev = nullptr;
   int64_t n2_cap = 0;
   double* small = nullptr;  // observe_reduce scratch (2 x 148 doubles)
+  unsigned long long* fixed_acc = nullptr;  // [3][dim] exact diagonal limbs (ctqw_observe_diag)
+  int64_t fixed_cap = 0;
   double* overlap_partial = nullptr;
   int64_t overlap_cap = 0;
   int64_t last_count = 0;
@@ -378,7 +380,7 @@ int ctqw_destroy(ctqw_handle_t h) {
   void* dev_ptrs[] = {h->levels, h->partial, h->scl, h->stats, h->events, h->fail,
                       h->summary_dev, h->scratch[0], h->scratch[1], h->n2_dev, h->small,
                       h->overlap_partial, h->tg_values, h->tg_next, h->tg_gen, h->tg_levels, h->tg_sum,
-                      h->lat_pos, h->lat_neg, h->t_slot, h->scratch_work};
+                      h->lat_pos, h->lat_neg, h->t_slot, h->scratch_work, h->fixed_acc};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (h->summary_host) cudaFreeHost(h->summary_host);
@@ -890,13 +892,40 @@ int ctqw_segment_stats(ctqw_handle_t h, int64_t r0, ctqw_segment_stats_t* out, v
   return CTQW_OK;
 }
 
+int ctqw_observe_diag_fixed(ctqw_handle_t h, const double* psi_dev, int64_t count, int64_t* acc_dev,
+                            int32_t accumulate, void* stream) {
+  if (!h || !acc_dev) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");
+  if (count < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative realization count");
+  if (count > 0 && !psi_dev) return fail_with(h, CTQW_ERR_CONFIG, "NULL state stack");
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, launch_observe_diag_fixed((const double2*)psi_dev, count, h->dim, (unsigned long long*)acc_dev,
+                                        accumulate != 0, (cudaStream_t)stream));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
+int ctqw_fixed_to_double(ctqw_handle_t h, const int64_t* acc_dev, double* diag_dev, void* stream) {
+  if (!h || !acc_dev || !diag_dev) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");
+  DeviceGuard g(h->device);
+  CUDA_TRY(h, launch_fixed_to_double((const unsigned long long*)acc_dev, h->dim, diag_dev, (cudaStream_t)stream));
+  h->launches += 1;
+  return CTQW_OK;
+}
+
 int ctqw_observe_diag(ctqw_handle_t h, const double* psi_dev, int64_t count, double* diag_sum_dev,
                       int32_t accumulate, void* stream) {
   if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
   DeviceGuard g(h->device);
-  CUDA_TRY(h, launch_observe_diag((const double2*)psi_dev, count, h->dim, diag_sum_dev,
-                                  accumulate != 0, (cudaStream_t)stream));
-  h->launches += 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = ensure(h, &h->fixed_acc, &h->fixed_cap, 3 * h->dim, "diagonal limbs");
+  if (rc) return rc;
+  if (accumulate) {
+    CUDA_TRY(h, launch_fixed_from_double(diag_sum_dev, h->dim, h->fixed_acc, s));
+    h->launches += 1;
+  }
+  CUDA_TRY(h, launch_observe_diag_fixed((const double2*)psi_dev, count, h->dim, h->fixed_acc, accumulate != 0, s));
+  CUDA_TRY(h, launch_fixed_to_double(h->fixed_acc, h->dim, diag_sum_dev, s));
+  h->launches += 2;
   return CTQW_OK;
 }
 

@@ -163,8 +163,10 @@ cudaError_t launch_norm_sum(const double* partial, int nparts, int64_t count, do
                             cudaStream_t s);
 cudaError_t launch_scale_rows(double2* psi, int64_t count, int64_t dim, const double* scl,
                               cudaStream_t s);
-cudaError_t launch_observe_diag(const double2* psi, int64_t count, int64_t dim, double* diag,
-                                bool accumulate, cudaStream_t s);
+cudaError_t launch_observe_diag_fixed(const double2* psi, int64_t count, int64_t dim, unsigned long long* acc,
+                                      bool accumulate, cudaStream_t s);
+cudaError_t launch_fixed_from_double(const double* diag, int64_t dim, unsigned long long* acc, cudaStream_t s);
+cudaError_t launch_fixed_to_double(const unsigned long long* acc, int64_t dim, double* diag, cudaStream_t s);
 cudaError_t launch_observe_reduce(int m, int n, int64_t dim, const double* diag_sum,
                                   double total, double* pops, double* scalars, double* joint,
                                   double* scratch, cudaStream_t s);

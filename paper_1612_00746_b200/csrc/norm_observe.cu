@@ -130,25 +130,98 @@ __global__ void norm_sum_kernel(const double* __restrict__ partial, int nparts, 
   n2[r] = s;
 }
 
-// diag[alpha] (+)= sum_r |psi_r(alpha)|^2 in realization order.
-__global__ void observe_diag_kernel(const double2* __restrict__ psi, int64_t count, int64_t dim,
-                                    double* diag, int accumulate) {
+// Exact (order-independent) ensemble sums of |psi_r(alpha)|^2.
+//
+// Each term x = |psi|^2 (x <= 2^22) is split, exactly and deterministically,
+// into three pieces on the fixed grids 2^-30, 2^-70 and 2^-110
+// (x = a2 + a1 + a0 + (rounding below 2^-111)), and each piece is added as an
+// int64 multiple of its grid: limb k of [3][dim].  Integer addition is
+// associative, so the sum is the same bits for any realization order, any
+// split of the realizations over blocks, atomics or GPUs (the all-reduce of
+// the limbs is an int64 SUM).  This is what makes the observables identical
+// across 1/2/4/8 GPUs, as the reference's are across worker counts
+// (pkg/README.md:174-180).  Limbs hold up to 2^23 realizations without
+// overflow.  Terms below 2^-111 (far beneath the 1e-10 relative bar on any
+// entry above 1e-30) are dropped.
+__device__ __forceinline__ void fixed_split(double x, long long& l2, long long& l1, long long& l0) {
+  const double c2 = 0x1.8p22, c1 = 0x1.8p-18, c0 = 0x1.8p-58;
+  const double a2 = __dsub_rn(__dadd_rn(x, c2), c2);  // nearest multiple of 2^-30
+  const double r1 = __dsub_rn(x, a2);                 // exact
+  const double a1 = __dsub_rn(__dadd_rn(r1, c1), c1); // nearest multiple of 2^-70
+  const double r0 = __dsub_rn(r1, a1);                // exact
+  const double a0 = __dsub_rn(__dadd_rn(r0, c0), c0); // nearest multiple of 2^-110
+  l2 = __double2ll_rn(__dmul_rn(a2, 0x1p30));
+  l1 = __double2ll_rn(__dmul_rn(a1, 0x1p70));
+  l0 = __double2ll_rn(__dmul_rn(a0, 0x1p110));
+}
+
+// acc[k][alpha] += sum_{r in this block's realization range} limb_k(|psi_r(alpha)|^2)
+__global__ void observe_diag_fixed_kernel(const double2* __restrict__ psi, int64_t count, int64_t dim,
+                                          int64_t rspan, unsigned long long* __restrict__ acc) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= dim) return;
-  double s = accumulate ? diag[a] : 0.0;
-  int64_t r = 0;
-  for (; r + 4 <= count; r += 4) {
-    const double2 v0 = __ldg(psi + (r + 0) * dim + a);
-    const double2 v1 = __ldg(psi + (r + 1) * dim + a);
-    const double2 v2 = __ldg(psi + (r + 2) * dim + a);
-    const double2 v3 = __ldg(psi + (r + 3) * dim + a);
-    s += norm2(v0);
-    s += norm2(v1);
-    s += norm2(v2);
-    s += norm2(v3);
+  const int64_t r0 = (int64_t)blockIdx.y * rspan;
+  const int64_t r1 = r0 + rspan < count ? r0 + rspan : count;
+  long long s2 = 0, s1 = 0, s0 = 0;
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = norm2(__ldg(psi + (r + u) * dim + a));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      long long l2, l1, l0;
+      fixed_split(v[u], l2, l1, l0);
+      s2 += l2;
+      s1 += l1;
+      s0 += l0;
+    }
   }
-  for (; r < count; ++r) s += norm2(__ldg(psi + r * dim + a));
-  diag[a] = s;
+  for (; r < r1; ++r) {
+    long long l2, l1, l0;
+    fixed_split(norm2(__ldg(psi + r * dim + a)), l2, l1, l0);
+    s2 += l2;
+    s1 += l1;
+    s0 += l0;
+  }
+  if (gridDim.y == 1) {
+    acc[a] += (unsigned long long)s2;
+    acc[dim + a] += (unsigned long long)s1;
+    acc[2 * dim + a] += (unsigned long long)s0;
+  } else {
+    atomicAdd(acc + a, (unsigned long long)s2);
+    atomicAdd(acc + dim + a, (unsigned long long)s1);
+    atomicAdd(acc + 2 * dim + a, (unsigned long long)s0);
+  }
+}
+
+// acc <- limbs of the doubles in diag (to accumulate onto an existing sum)
+__global__ void fixed_from_double_kernel(const double* __restrict__ diag, int64_t dim,
+                                         unsigned long long* __restrict__ acc) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= dim) return;
+  long long l2, l1, l0;
+  fixed_split(diag[a], l2, l1, l0);
+  acc[a] = (unsigned long long)l2;
+  acc[dim + a] = (unsigned long long)l1;
+  acc[2 * dim + a] = (unsigned long long)l0;
+}
+
+// diag[alpha] = value of the limbs: carries normalised in integers, then
+// L2 * 2^-30 (exact) + (L1 * 2^-70 + L0 * 2^-110) (one rounding each).
+__global__ void fixed_to_double_kernel(const unsigned long long* __restrict__ acc, int64_t dim,
+                                       double* __restrict__ diag) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= dim) return;
+  long long l2 = (long long)acc[a], l1 = (long long)acc[dim + a], l0 = (long long)acc[2 * dim + a];
+  const long long c0 = l0 >> 40;  // floor
+  l0 -= c0 << 40;
+  l1 += c0;
+  const long long c1 = l1 >> 40;
+  l1 -= c1 << 40;
+  l2 += c1;
+  const double lo = __dadd_rn(__dmul_rn((double)l1, 0x1p-70), __dmul_rn((double)l0, 0x1p-110));
+  diag[a] = __dadd_rn(__dmul_rn((double)l2, 0x1p-30), lo);
 }
 
 // populations[x] = sum_p sum_{alpha: x_p = x} p(alpha), p = diag/total.
@@ -339,11 +412,36 @@ cudaError_t launch_norm_sum(const double* partial, int nparts, int64_t count, do
   return cudaGetLastError();
 }
 
-cudaError_t launch_observe_diag(const double2* psi, int64_t count, int64_t dim, double* diag,
-                                bool accumulate, cudaStream_t s) {
+cudaError_t launch_observe_diag_fixed(const double2* psi, int64_t count, int64_t dim, unsigned long long* acc,
+                                      bool accumulate, cudaStream_t s) {
+  if (!accumulate) {
+    cudaError_t e = cudaMemsetAsync(acc, 0, (size_t)3 * dim * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+  }
+  if (count <= 0 || dim <= 0) return cudaSuccess;
   const int bs = 256;
-  observe_diag_kernel<<<(unsigned)((dim + bs - 1) / bs), bs, 0, s>>>(psi, count, dim, diag,
-                                                                      accumulate ? 1 : 0);
+  const int64_t bx = (dim + bs - 1) / bs;
+  // enough blocks to fill the GPU: split the realizations over blockIdx.y
+  // (exact integer atomics make the split invisible in the result)
+  int64_t ny = (4 * 148 + bx - 1) / bx;
+  if (ny > count) ny = count;
+  if (ny > 65535) ny = 65535;
+  if (ny < 1) ny = 1;
+  const int64_t rspan = (count + ny - 1) / ny;
+  ny = (count + rspan - 1) / rspan;
+  observe_diag_fixed_kernel<<<dim3((unsigned)bx, (unsigned)ny), bs, 0, s>>>(psi, count, dim, rspan, acc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fixed_from_double(const double* diag, int64_t dim, unsigned long long* acc, cudaStream_t s) {
+  if (dim <= 0) return cudaSuccess;
+  fixed_from_double_kernel<<<(unsigned)((dim + 255) / 256), 256, 0, s>>>(diag, dim, acc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fixed_to_double(const unsigned long long* acc, int64_t dim, double* diag, cudaStream_t s) {
+  if (dim <= 0) return cudaSuccess;
+  fixed_to_double_kernel<<<(unsigned)((dim + 255) / 256), 256, 0, s>>>(acc, dim, diag);
   return cudaGetLastError();
 }
 

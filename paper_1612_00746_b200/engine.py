@@ -340,7 +340,10 @@ class EnsembleState:
         space = config.space
         self.topology = build_topology(space)
         model = config.model
-        self.handle = model_handle(self.topology, model, device=device)
+        # a private handle: this ensemble's coefficient rows and telegraph
+        # process stay bound for the whole run, whatever the caller does with
+        # the cached handles of the single-step API in between
+        self.handle = model_handle(self.topology, model, device=device, private=True)
         self.dev = torch.device(f"cuda:{device}")
         n = space.lattice.n_sites
         self.dynamic = not config.noise.is_static
@@ -411,6 +414,11 @@ class EnsembleState:
     def diagonal_sum(self, out):
         self.handle.observe_diag(self.psi, self.count, out, accumulate=False)
         return out
+
+    def diagonal_limbs(self, acc):
+        """acc[3][D] int64 = exact fixed-point limbs of this shard's sum_r |psi_r|^2."""
+        self.handle.observe_diag_fixed(self.psi, self.count, acc, accumulate=False)
+        return acc
 
     def states(self):
         return self.psi[: self.count]
@@ -504,12 +512,13 @@ def collect_observables_async(config, ens: EnsembleState, group=None, want_joint
     space = config.space
     dim = space.dim
     n = space.lattice.n_sites
+    # exact int64 limbs: the all-reduce (and so every row) is bitwise the same
+    # for any number of ranks and any split of the realizations
+    acc = torch.empty((3, dim), dtype=torch.int64, device=ens.dev)
+    ens.diagonal_limbs(acc)
+    sharding.allreduce_sum_(acc, group)
     diag = torch.empty(dim, dtype=torch.float64, device=ens.dev)
-    if ens.count:
-        ens.diagonal_sum(diag)
-    else:
-        diag.zero_()
-    sharding.allreduce_sum_(diag, group)
+    ens.handle.fixed_to_double(acc, diag)
     packed = torch.zeros(n + 4, dtype=torch.float64, device=ens.dev)
     need_joint = OBS_JOINT in config.observables if want_joint is None else want_joint
     joint = torch.empty(dim, dtype=torch.float64, device=ens.dev) if need_joint else None
@@ -595,7 +604,7 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
             t_obs1 = clock()
             if span > 0:
                 local = ens.stats()
-                merged = sharding.merge_segment_stats(sharding.gather_objects(local, group))
+                merged = sharding.merge_segment_stats(sharding.gather_stats(local, group))
                 profile.add(STAGE_EVOLUTION, (t_ev - t0) + (clock() - t_obs1),
                             calls=config.realizations * span)
                 # the Hamiltonian is generated on the fly; dynamic noise rewrites the
@@ -633,7 +642,7 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
             emit(sinks.density_snapshot, rho, target)
 
     with torch.cuda.device(device):
-        switches = sum(sharding.gather_objects(ens.switch_count(), group))
+        switches = sharding.allreduce_int_([ens.switch_count()], group)[0]
     report = RunReport(config=config, profile=profile, io_seconds=io_seconds,
                        wall_seconds=clock() - wall_start, workers=world, snapshots=snapshots,
                        max_norm_deviation=max_deviation, norm_corrections=corrections,

@@ -73,17 +73,32 @@ def handle_for(m, n, onsite, tunneling, interaction, hbar, device=None, lattice=
     return h
 
 
-def model_handle(topology, model: CouplingModel, hbar=None, device=None):
+def model_handle(topology, model: CouplingModel, hbar=None, device=None, private: bool = False):
     """Handle for ``topology`` + ``model``: the ring as is, any other lattice
     with its move tables and the tunnelling of each slot's direction
-    (slot_couplings, hamiltonian.py:92-97)."""
+    (slot_couplings, hamiltonian.py:92-97).
+
+    ``private=True`` returns a new, uncached handle: an ensemble binds its own
+    coefficient rows and telegraph process into its handle, so it must not
+    share one with the single-step API or another ensemble."""
+    import torch
+
+    from .native import Handle
+
     hb = model.hbar if hbar is None else hbar
     if topology.is_ring:
-        return handle_for(topology.m, topology.n, model.onsite_energy, model.ring_tunneling(),
-                          model.interaction, hb, device)
+        args = (topology.m, topology.n, model.onsite_energy, model.ring_tunneling(), model.interaction, hb)
+        if private:
+            dev = torch.cuda.current_device() if device is None else device
+            return Handle(*args, dev)
+        return handle_for(*args, device)
     lat = topology.lattice
     pos, neg, directions = topology.move_tables()
     t_slot = model.tunneling_per_direction(lat.q)[directions]
+    if private:
+        dev = torch.cuda.current_device() if device is None else device
+        return Handle(topology.m, topology.n, model.onsite_energy, float(t_slot[0]), model.interaction, hb, dev,
+                      lattice=(pos, neg, t_slot))
     key = (lat.dims, lat.k_half, lat.boundary, tuple(float(v) for v in t_slot))
     return handle_for(topology.m, topology.n, model.onsite_energy, float(t_slot[0]), model.interaction, hb,
                       device, lattice=(pos, neg, t_slot), lattice_key=key)

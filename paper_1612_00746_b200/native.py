@@ -103,6 +103,8 @@ SIGNATURES = {
                                    ctypes.POINTER(_I32), _P]),
     "ctqw_segment_stats": (ctypes.c_int, [_P, _I64, ctypes.POINTER(SegmentStats), _P]),
     "ctqw_observe_diag": (ctypes.c_int, [_P, _P, _I64, _P, _I32, _P]),
+    "ctqw_observe_diag_fixed": (ctypes.c_int, [_P, _P, _I64, _P, _I32, _P]),
+    "ctqw_fixed_to_double": (ctypes.c_int, [_P, _P, _P, _P]),
     "ctqw_observe_reduce": (ctypes.c_int, [_P, _P, _D, _P, _P, _P, _P]),
     "ctqw_overlap_sumsq": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
     "ctqw_launch_count": (ctypes.c_int64, [_P]),
@@ -323,6 +325,14 @@ class Handle:
     def observe_diag(self, psi, count: int, diag_sum, accumulate: bool = False):
         self._check(self.lib.ctqw_observe_diag(self._h, _ptr(psi), int(count), _ptr(diag_sum),
                                                1 if accumulate else 0, self.stream))
+
+    def observe_diag_fixed(self, psi, count: int, acc, accumulate: bool = False):
+        """acc[3][D] (int64) (+)= exact limbs of sum_r |psi_r|^2 (order independent)."""
+        self._check(self.lib.ctqw_observe_diag_fixed(self._h, _ptr(psi) if count else None, int(count), _ptr(acc),
+                                                     int(bool(accumulate)), self.stream))
+
+    def fixed_to_double(self, acc, diag):
+        self._check(self.lib.ctqw_fixed_to_double(self._h, _ptr(acc), _ptr(diag), self.stream))
 
     def observe_reduce(self, diag_sum, total: float, pops, scalars, joint=None):
         self._check(self.lib.ctqw_observe_reduce(self._h, _ptr(diag_sum), float(total), _ptr(pops),

@@ -5,8 +5,10 @@ The reference parallelises only over realizations: contiguous chunks from
 host concatenates the chunk states to average them (ensemble.py:762-768).
 Here each rank owns a contiguous realization shard for the whole run
 (states never move between GPUs); the only cross-GPU traffic is, at each
-post-processing point, an all-reduce of the per-rank diagonal partial sums
-(NCCL over NVLink) plus a tiny all-gather of the per-rank norm statistics.
+post-processing point, an all-reduce of the per-rank diagonal sums -- exact
+int64 fixed-point limbs, so the result is bitwise the same for any number of
+ranks -- (NCCL over NVLink) plus one all-gather of a fixed-size tensor of the
+per-rank norm statistics.
 Purity, which needs overlaps between realizations on different ranks, is the
 one exception and gathers the states (small problems only).
 
@@ -58,8 +60,20 @@ def allreduce_sum_(tensor, group=None):
     return tensor
 
 
+def _comm_device(group=None):
+    """Tensors for collectives live on the current CUDA device under NCCL, on
+    the host under gloo (the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def gather_objects(obj, group=None):
-    """List of ``obj`` from every rank in rank order."""
+    """List of ``obj`` from every rank in rank order (small host-side objects,
+    not on the per-collection-point path)."""
     import torch.distributed as dist
 
     if _collective(group):
@@ -69,25 +83,95 @@ def gather_objects(obj, group=None):
     return [obj]
 
 
+def allreduce_int_(values, group=None):
+    """Sum of a few host integers over ranks (one int64 tensor all-reduce)."""
+    import torch
+    import torch.distributed as dist
+
+    if not _collective(group):
+        return [int(v) for v in values]
+    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=_comm_device(group))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return [int(v) for v in t.cpu().tolist()]
+
+
+MAX_EVENTS = 100
+_HEAD = 8  # event_count, corrections, max_deviation, failed, fail_dev, fail_real, fail_step, n_events
+
+
+def pack_stats(st) -> list:
+    """Fixed-size float64 record of one rank's segment statistics (counts and
+    indices stay exact below 2^53)."""
+    fail = st["failure"]
+    events = list(st["events"])[:MAX_EVENTS]
+    rec = [float(st["event_count"]), float(st["corrections"]), float(st["max_deviation"]),
+           1.0 if fail is not None else 0.0,
+           float(fail[0]) if fail else 0.0, float(fail[1]) if fail else 0.0, float(fail[2]) if fail else 0.0,
+           float(len(events))]
+    for dev, corrected, real, step in events:
+        rec.extend((float(dev), 1.0 if corrected else 0.0, float(real), float(step)))
+    rec.extend([0.0] * (4 * (MAX_EVENTS - len(events))))
+    return rec
+
+
+def unpack_stats(rec) -> dict:
+    rec = [float(v) for v in rec]
+    n_ev = int(rec[7])
+    events = []
+    for k in range(n_ev):
+        dev, corr, real, step = rec[_HEAD + 4 * k: _HEAD + 4 * k + 4]
+        events.append((dev, bool(corr), int(real), int(step)))
+    failure = (rec[4], int(rec[5]), int(rec[6])) if rec[3] else None
+    return {"event_count": int(rec[0]), "corrections": int(rec[1]), "max_deviation": rec[2],
+            "events": events, "failure": failure}
+
+
+def gather_stats(local, group=None):
+    """Every rank's segment statistics, in rank order: ONE all-gather of a
+    fixed-size float64 tensor (8 + 4*MAX_EVENTS entries per rank)."""
+    import torch
+    import torch.distributed as dist
+
+    if not _collective(group):
+        return [local]
+    dev = _comm_device(group)
+    mine = torch.tensor(pack_stats(local), dtype=torch.float64, device=dev)
+    bufs = [torch.empty_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(bufs, mine, group=group)
+    return [unpack_stats(b.cpu().tolist()) for b in bufs]
+
+
 def merge_segment_stats(per_rank):
-    """Combine per-rank segment statistics like the reference combines chunks.
+    """Combine per-rank segment statistics independently of how the
+    realizations were split.
 
     ``per_rank`` is a list (rank order) of dicts with keys event_count,
-    corrections, max_deviation, events (list of tuples) and failure (None or
-    (deviation, realization, step)).  Totals add, the maximum deviation is
-    the max, events concatenate in shard order (ensemble.py:751-758), and the
-    failure reported is the first shard's that failed -- the reference
-    collects chunk futures in order (ensemble.py:727-730).
+    corrections, max_deviation, events (list of (dev, corrected, realization,
+    step)) and failure (None or (deviation, realization, step)).  Totals
+    add, the maximum deviation is the max, the events kept are the first
+    MAX_EVENTS in (step, realization) order -- each rank's list holds its own
+    first MAX_EVENTS in that order, so the union contains the global first
+    ones -- and the failure reported is the one a single process reports
+    (the device reduction's rule): earliest step, then largest deviation,
+    then lowest realization.  So 1, 2, 4 or 8 GPUs report the same events and
+    the same culprit (the reference's single-chunk semantics,
+    propagators.py:320-323, ensemble.py:503-516).
     """
     merged = {"event_count": 0, "corrections": 0, "max_deviation": 0.0, "events": [],
               "failure": None}
+    events = []
     for st in per_rank:
         merged["event_count"] += int(st["event_count"])
         merged["corrections"] += int(st["corrections"])
         merged["max_deviation"] = max(merged["max_deviation"], float(st["max_deviation"]))
-        merged["events"].extend(st["events"])
-        if merged["failure"] is None and st["failure"] is not None:
-            merged["failure"] = st["failure"]
+        events.extend(st["events"])
+        f = st["failure"]
+        if f is not None:
+            cur = merged["failure"]
+            if cur is None or (f[2], -f[0], f[1]) < (cur[2], -cur[0], cur[1]):
+                merged["failure"] = (float(f[0]), int(f[1]), int(f[2]))
+    events.sort(key=lambda e: (e[3], e[2]))
+    merged["events"] = events[:MAX_EVENTS]
     return merged
 
 
@@ -98,7 +182,10 @@ def gather_states(local, group=None):
 
     if not _collective(group):
         return local
-    sizes = gather_objects(int(local.shape[0]), group)
+    cnt = torch.tensor([int(local.shape[0])], dtype=torch.int64, device=_comm_device(group))
+    cnts = [torch.empty_like(cnt) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(cnts, cnt, group=group)
+    sizes = [int(c.item()) for c in cnts]
     flat = torch.view_as_real(local) if local.is_complex() else local
     biggest = max(sizes)
     padded = torch.zeros((biggest,) + tuple(flat.shape[1:]), dtype=flat.dtype, device=flat.device)
@@ -109,5 +196,5 @@ def gather_states(local, group=None):
     return torch.view_as_complex(out) if local.is_complex() else out
 
 
-__all__ = ["world_info", "shard_bounds", "all_shards", "allreduce_sum_", "gather_objects",
-           "merge_segment_stats", "gather_states"]
+__all__ = ["world_info", "shard_bounds", "all_shards", "allreduce_sum_", "allreduce_int_", "gather_objects",
+           "gather_stats", "pack_stats", "unpack_stats", "merge_segment_stats", "gather_states"]

@@ -756,3 +756,38 @@ def test_plane3_in_place_run_capacity(pkg):
                       precision="double", memory_budget=200 * 2**30)
     assert marches_in_place(cfg)
     assert estimate_memory(cfg)["state_bytes"] == 5000 * 2**21 * 16
+
+
+# ---------------------------------------------------------------------------
+# exact diagonal accumulation (int64 limbs): bitwise vs the NumPy restatement,
+# independent of order and batching
+
+
+def test_observe_diag_fixed_limbs_bitwise(pkg):
+    from tests import fixed_point as fx
+
+    rng = np.random.default_rng(3)
+    for R, n in ((37, 24), (5, 256), (300, 16)):
+        dim = n * n
+        psi = random_states(R, dim, seed=R) * rng.uniform(0.5, 2.0, size=(R, 1))
+        h = make_handle(2, n)
+        dev = to_dev(psi)
+        acc = torch.empty((3, dim), dtype=torch.int64, device="cuda:0")
+        h.observe_diag_fixed(dev, R, acc)
+        ref = fx.limbs(psi)
+        np.testing.assert_array_equal(acc.cpu().numpy(), ref)
+        # any order / split of the realizations gives the same limbs
+        acc2 = torch.empty_like(acc)
+        h.observe_diag_fixed(to_dev(psi[::-1]), R, acc2)
+        np.testing.assert_array_equal(acc2.cpu().numpy(), ref)
+        h.observe_diag_fixed(to_dev(psi[: R // 2]), R // 2, acc2)
+        h.observe_diag_fixed(to_dev(psi[R // 2:]), R - R // 2, acc2, accumulate=True)
+        np.testing.assert_array_equal(acc2.cpu().numpy(), ref)
+        diag = torch.empty(dim, dtype=torch.float64, device="cuda:0")
+        h.fixed_to_double(acc, diag)
+        np.testing.assert_array_equal(diag.cpu().numpy(), fx.to_double(ref))
+        # the double API is the same sum
+        d2 = torch.empty_like(diag)
+        h.observe_diag(dev, R, d2)
+        np.testing.assert_array_equal(d2.cpu().numpy(), diag.cpu().numpy())
+        np.testing.assert_allclose(diag.cpu().numpy(), (np.abs(psi) ** 2).sum(axis=0), rtol=1e-15)

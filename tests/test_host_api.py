@@ -208,7 +208,10 @@ def test_shard_bounds_cover_realizations():
             assert max(sizes) - min(sizes) <= 1
 
 
-def test_merge_stats_first_failing_shard_wins():
+def test_merge_stats_is_split_independent():
+    """Failure = earliest step, then largest deviation, then lowest
+    realization; events = first MAX_EVENTS in (step, realization) order --
+    the same answer a single process gives, whatever the shard split."""
     a = {"event_count": 2, "corrections": 2, "max_deviation": 3e-6, "events": [(3e-6, True, 1, 5)],
          "failure": None}
     b = {"event_count": 1, "corrections": 1, "max_deviation": 2e-6, "events": [(2e-6, True, 9, 2)],
@@ -217,5 +220,22 @@ def test_merge_stats_first_failing_shard_wins():
     m = sharding.merge_segment_stats([a, b, c])
     assert m["event_count"] == 3 and m["corrections"] == 3
     assert m["max_deviation"] == 3e-6
-    assert m["events"] == [(3e-6, True, 1, 5), (2e-6, True, 9, 2)]
-    assert m["failure"] == (5e-3, 9, 4)
+    assert m["events"] == [(2e-6, True, 9, 2), (3e-6, True, 1, 5)]
+    assert m["failure"] == (9e-3, 12, 1)
+    # same step: the larger deviation, then the lower realization
+    d = {"event_count": 0, "corrections": 0, "max_deviation": 0.0, "events": [], "failure": (9e-3, 3, 1)}
+    e = {"event_count": 0, "corrections": 0, "max_deviation": 0.0, "events": [], "failure": (8e-3, 1, 1)}
+    assert sharding.merge_segment_stats([c, e, d])["failure"] == (9e-3, 3, 1)
+    # order of the ranks does not matter
+    assert sharding.merge_segment_stats([c, b, a]) == m
+
+
+def test_stats_pack_roundtrip():
+    st = {"event_count": 250, "corrections": 7, "max_deviation": 1.5e-6,
+          "events": [(1e-6 * k, k % 2 == 0, 1000 + k, 3 + k // 10) for k in range(100)],
+          "failure": (2e-3, 123456789, 42)}
+    rec = sharding.pack_stats(st)
+    assert len(rec) == 8 + 4 * sharding.MAX_EVENTS
+    assert sharding.unpack_stats(rec) == st
+    st2 = dict(st, events=[], failure=None)
+    assert sharding.unpack_stats(sharding.pack_stats(st2)) == st2
