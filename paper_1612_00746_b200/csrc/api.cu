@@ -79,7 +79,9 @@ struct ctqw_ctx {
   double tg_mean_wait = 0.0;
   bool tg_enabled = false;
   long long* tg_sum = nullptr;
-  int stream_kind = 0;  // CTQW_STREAM: 0 auto, 1 tile, 2 band, 3 band2, 4 band4, 5 plane3, 6 generic
+  int* tg_lists = nullptr;          // [count][2][total] due lists (advance scratch)
+  double* tg_oldv = nullptr;        // [count][total] values before the advance
+  int stream_kind = 0;  // CTQW_STREAM: 0 auto, 1 tile, 4 band4, 5 plane3, 6 generic
   const char* stream_kernel = "";  // dominant kernel of the last ctqw_evolve
   char variant[128] = {0};         // its compile-time specialization (ctqw_step_variant)
   std::string err;
@@ -292,7 +294,7 @@ int telegraph_step(ctqw_ctx* h, int64_t count, double dt, cudaStream_t s) {
   CUDA_TRY(h, launch_telegraph_advance(count, h->tg_total, h->tg_links, h->tg_sites, h->n, dt, h->tg_levels,
                                        h->tg_nlev, h->tg_mean_wait, h->t_slot, h->K, h->tg_values, h->tg_next,
                                        h->tg_gen, const_cast<double*>(h->hop), const_cast<double*>(h->site),
-                                       h->stride, h->site_stride, h->fail, s));
+                                       h->stride, h->site_stride, h->tg_lists, h->tg_oldv, h->fail, s));
   h->launches += 1;
   return CTQW_OK;
 }
@@ -362,8 +364,6 @@ int ctqw_create(const ctqw_model_t* model, int32_t device, ctqw_handle_t* out) {
   cudaMemcpy(h->t_slot, &md.tunneling, sizeof(double), cudaMemcpyHostToDevice);
   if (const char* sk = std::getenv("CTQW_STREAM")) {
     h->stream_kind = std::strcmp(sk, "tile") == 0    ? 1
-                     : std::strcmp(sk, "band") == 0  ? 2
-                     : std::strcmp(sk, "band2") == 0 ? 3
                      : std::strcmp(sk, "band4") == 0 ? 4
                      : std::strcmp(sk, "plane3") == 0 ? 5
                      : std::strcmp(sk, "generic") == 0 ? 6
@@ -380,7 +380,8 @@ int ctqw_destroy(ctqw_handle_t h) {
   void* dev_ptrs[] = {h->levels, h->partial, h->scl, h->stats, h->events, h->fail,
                       h->summary_dev, h->scratch[0], h->scratch[1], h->n2_dev, h->small,
                       h->overlap_partial, h->tg_values, h->tg_next, h->tg_gen, h->tg_levels, h->tg_sum,
-                      h->lat_pos, h->lat_neg, h->t_slot, h->scratch_work, h->fixed_acc};
+                      h->lat_pos, h->lat_neg, h->t_slot, h->scratch_work, h->fixed_acc,
+                      h->tg_lists, h->tg_oldv};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (h->summary_host) cudaFreeHost(h->summary_host);
@@ -433,6 +434,13 @@ int ctqw_telegraph_init(ctqw_handle_t h, uint64_t master_seed, int64_t r0, int64
   h->tg_gen = nullptr;
   if (count > 0 && cudaMalloc(&h->tg_gen, count * sizeof(TelegraphGen)) != cudaSuccess)
     return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate telegraph generators");
+  for (void** p : {(void**)&h->tg_lists, (void**)&h->tg_oldv}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  if (count * total > 0 && (cudaMalloc(&h->tg_lists, (size_t)count * total * 2 * sizeof(int)) != cudaSuccess ||
+                            cudaMalloc(&h->tg_oldv, (size_t)count * total * sizeof(double)) != cudaSuccess))
+    return fail_with(h, CTQW_ERR_CAPACITY, "cannot allocate the telegraph due lists");
   if (h->tg_levels) cudaFree(h->tg_levels);
   h->tg_levels = nullptr;
   if (cudaMalloc(&h->tg_levels, n_levels * sizeof(double)) != cudaSuccess)
@@ -466,7 +474,7 @@ int ctqw_telegraph_advance(ctqw_handle_t h, int64_t count, double dt, void* stre
                                        h->tg_nlev, h->tg_mean_wait, h->t_slot, h->K, h->tg_values, h->tg_next,
                                        h->tg_gen, coef ? const_cast<double*>(h->hop) : nullptr,
                                        coef ? const_cast<double*>(h->site) : nullptr, h->stride, h->site_stride,
-                                       nullptr, (cudaStream_t)stream));
+                                       h->tg_lists, h->tg_oldv, nullptr, (cudaStream_t)stream));
   h->launches += 1;
   return CTQW_OK;
 }
@@ -728,21 +736,16 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
     work = h->scratch_work;
   }
   if (!work) work = psi;
-  // streaming m = 2 path: the four-column band kernel by default; the older
-  // band / band2 / tile kernels stay selectable for A/B measurements
-  // CTQW_STREAM pins one kernel family (A/B measurements, per-kernel parity
-  // tests); a pinned family that does not support the case falls through
-  // to the next one in auto order.
+  // streaming m = 2 path: the four-column band kernel (N % 4 == 0, N <= 1024);
+  // the tile kernel covers the other m = 2 sizes.  CTQW_STREAM pins one
+  // family (A/B measurements, per-kernel parity tests); a pinned family that
+  // does not support the case falls through to the next one in auto order.
   const int kind = h->general ? 6 : h->stream_kind;
   const bool use_band4 = (kind == 0 || kind == 4) && band4_supported(h->m, h->n, sc);
   const bool use_plane3 = (kind == 0 || kind == 5) && plane3_supported(h->m, h->n, sc);
-  const bool use_band2 = !use_band4 && (kind == 0 || kind == 3 || kind == 4) &&
-                         band2_supported(h->m, h->n, sc, exact, kind == 3);
-  const bool use_band = !use_band4 && !use_band2 && kind != 1 && kind < 5 && band_supported(h->m, h->n, sc);
-  const bool use_tile = !use_band4 && !use_band2 && !use_band && kind < 5 && tile_supported(h->m, h->n, sc);
-  if (use_plane3 || use_band4 || use_band2 || use_band || use_tile) {
-    h->stream_kernel = use_plane3 ? "plane3_kernel" : use_band4 ? "band4_kernel" : use_band2 ? "band2_kernel"
-                       : use_band ? "band_ws_kernel" : "tile_step_kernel";
+  const bool use_tile = !use_band4 && kind < 5 && tile_supported(h->m, h->n, sc);
+  if (use_plane3 || use_band4 || use_tile) {
+    h->stream_kernel = use_plane3 ? "plane3_kernel" : use_band4 ? "band4_kernel" : "tile_step_kernel";
     {
       const int napp = sc.backend == CTQW_BACKEND_RK4 ? 4 : sc.order;
       // band4 compiles N in for the four-application steps at the BASELINE sizes
@@ -754,8 +757,6 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
     }
     const int nparts = use_plane3 ? plane3_parts()
                        : use_band4 ? band4_parts(h->n)
-                       : use_band2 ? band2_parts(h->n, sc, coef.site != nullptr, count)
-                       : use_band ? band_parts(h->n, sc, coef.site != nullptr, count)
                                   : tile_parts(h->n, sc);
     rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
     if (rc) return rc;
@@ -770,12 +771,6 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       else if (use_band4)
         CUDA_TRY(h, launch_band4_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
                                       h->fail, s));
-      else if (use_band2)
-        CUDA_TRY(h, launch_band2_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
-                                      h->fail, s));
-      else if (use_band)
-        CUDA_TRY(h, launch_band_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
-                                     h->fail, s));
       else
         CUDA_TRY(h, launch_tile_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
                                      h->fail, s));

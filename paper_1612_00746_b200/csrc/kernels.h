@@ -67,12 +67,12 @@ struct TelegraphGen {
 cudaError_t launch_telegraph_init(uint64_t master_seed, int64_t r0, int64_t count, const double* levels_dev,
                                   int n_levels, int64_t total, double mean_wait, double* values,
                                   double* next_switch, TelegraphGen* gen, cudaStream_t s);
-size_t telegraph_advance_smem(int64_t total);
 cudaError_t launch_telegraph_advance(int64_t count, int64_t total, int64_t n_links, int64_t n_sites, int n,
                                      double dt, const double* levels_dev, int n_levels, double mean_wait,
                                      const double* t_slot, int K, double* values, double* next_switch,
                                      TelegraphGen* gen, double* hop, double* site, int64_t hop_stride,
-                                     int64_t site_stride, const long long* fail, cudaStream_t s);
+                                     int64_t site_stride, int* lists, double* oldv, const long long* fail,
+                                     cudaStream_t s);
 
 // stencil_generic.cu
 cudaError_t launch_apply(int m, const double2* psi, double2* out, int64_t count, int64_t dim,
@@ -120,20 +120,6 @@ cudaError_t launch_band4_step(const double2* psi_in, double2* psi_out, int64_t c
                               const Coef& coef, const StencilConst& k, const StepScalars& sc,
                               bool exact, const double* scl, double* partial,
                               const long long* fail, cudaStream_t s);
-// step_band2.cu (m = 2 row-marching kernel, two columns per thread)
-bool band2_supported(int m, int n, const StepScalars& sc, bool exact, bool force);
-int band2_parts(int n, const StepScalars& sc, bool site, int64_t count);
-cudaError_t launch_band2_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
-                              const Coef& coef, const StencilConst& k, const StepScalars& sc,
-                              bool exact, const double* scl, double* partial,
-                              const long long* fail, cudaStream_t s);
-// step_band.cu (m = 2 row-marching streaming kernel)
-bool band_supported(int m, int n, const StepScalars& sc);
-int band_parts(int n, const StepScalars& sc, bool site, int64_t count);
-cudaError_t launch_band_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
-                             const Coef& coef, const StencilConst& k, const StepScalars& sc,
-                             bool exact, const double* scl, double* partial,
-                             const long long* fail, cudaStream_t s);
 cudaError_t launch_resident(double2* psi, int64_t count, int n, const Coef& coef,
                             const StencilConst& k, const StepScalars& sc, bool exact,
                             const NormPolicy& pol, long long first_step, long long n_steps,

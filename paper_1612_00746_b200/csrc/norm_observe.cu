@@ -277,7 +277,9 @@ __global__ void joint_final_kernel(const double* __restrict__ partial, int npart
   scalars[0] = s1;
   scalars[1] = s2;
   // participation ratio 1 / sum (p/S1)^2 = S1^2 / S2  (observables.py:94-101)
-  scalars[2] = s2 > 0.0 ? (s1 * s1) / s2 : 0.0;
+  // NaN states give NaN; a zero-weight distribution gives NaN too and the
+  // host raises NumericError on s2 <= 0, as observables.py:98-99 does
+  scalars[2] = s2 > 0.0 ? (s1 * s1) / s2 : (s2 == s2 ? __longlong_as_double(0x7ff8000000000000LL) : s2);
 }
 
 // sum_{i,j} |<a_i|b_j>|^2 : 32 x 32 tiles of the overlap matrix G = A^H B,

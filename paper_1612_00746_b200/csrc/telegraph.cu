@@ -62,21 +62,23 @@ __global__ void telegraph_init_kernel(uint64_t master_seed, int64_t r0, int64_t 
 
 constexpr int kAdvWarps = 4;
 
-// idx lists live in shared memory: [kAdvWarps][2][total] ints (current list,
-// and the original due list whose old values decide "changed").
+// Per-realization due lists in a global scratch owned by the handle:
+// lists[r] = [current list | original due list] (2 x total ints) and
+// oldv[r] = the original values (total doubles), whose comparison with the
+// new values decides "changed".  Global (L1/L2-resident) rather than shared
+// memory, so any lattice size works (N*K + N elements per realization).
 __global__ void __launch_bounds__(32 * kAdvWarps) telegraph_advance_kernel(
     int64_t count, int64_t total, int64_t n_links, int64_t n_sites, int n, double dt,
     const double* __restrict__ levels, int n_levels, double mean_wait, const double* __restrict__ t_slot, int K,
     double* __restrict__ values, double* __restrict__ next_switch, TelegraphGen* __restrict__ gen,
     double* __restrict__ hop, double* __restrict__ site, int64_t hop_stride, int64_t site_stride,
-    const long long* fail) {
-  extern __shared__ int adv_smem[];
+    int* __restrict__ lists, double* __restrict__ oldv_all, const long long* fail) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * kAdvWarps + warp;
   if (r >= count || (fail && *fail != kNoFail)) return;
-  int* cur = adv_smem + (int64_t)warp * 3 * total;
+  int* cur = lists + r * 2 * total;
   int* orig = cur + total;
-  double* oldv = reinterpret_cast<double*>(adv_smem + (int64_t)kAdvWarps * 3 * total) + (int64_t)warp * total;
+  double* oldv = oldv_all + r * total;
   TelegraphGen t = gen[r];
   const double t_end = __dadd_rn(t.time, dt);
   double* v = values + r * total;
@@ -157,28 +159,16 @@ cudaError_t launch_telegraph_init(uint64_t master_seed, int64_t r0, int64_t coun
   return cudaGetLastError();
 }
 
-size_t telegraph_advance_smem(int64_t total) {
-  return (size_t)kAdvWarps * total * (3 * sizeof(int) + sizeof(double));
-}
-
 cudaError_t launch_telegraph_advance(int64_t count, int64_t total, int64_t n_links, int64_t n_sites, int n,
                                      double dt, const double* levels_dev, int n_levels, double mean_wait,
                                      const double* t_slot, int K, double* values, double* next_switch,
                                      TelegraphGen* gen, double* hop, double* site, int64_t hop_stride,
-                                     int64_t site_stride, const long long* fail, cudaStream_t s) {
+                                     int64_t site_stride, int* lists, double* oldv, const long long* fail,
+                                     cudaStream_t s) {
   if (count <= 0 || total <= 0) return cudaSuccess;
-  const size_t smem = telegraph_advance_smem(total);
-  static size_t configured[64] = {};
-  size_t& conf = configured[current_device() & 63];
-  if (smem > 48 * 1024 && smem > conf) {
-    cudaError_t e = cudaFuncSetAttribute(telegraph_advance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    conf = smem;
-  }
-  telegraph_advance_kernel<<<(unsigned)((count + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps, smem, s>>>(
+  telegraph_advance_kernel<<<(unsigned)((count + kAdvWarps - 1) / kAdvWarps), 32 * kAdvWarps, 0, s>>>(
       count, total, n_links, n_sites, n, dt, levels_dev, n_levels, mean_wait, t_slot, K, values, next_switch, gen,
-      hop, site, hop_stride, site_stride, fail);
+      hop, site, hop_stride, site_stride, lists, oldv, fail);
   return cudaGetLastError();
 }
 

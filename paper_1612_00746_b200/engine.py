@@ -29,7 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import sharding
-from .errors import CapacityError, ConfigurationError, MemoryBudgetError, NormFailureError
+from .errors import CapacityError, ConfigurationError, MemoryBudgetError, NormFailureError, NumericError
 from .geometry import JointSpace, build_topology, joint_index
 from .hamiltonian import CouplingModel, handle_for, model_handle
 from .noise import NoiseSpec, draw_noise
@@ -209,40 +209,79 @@ class RunConfig:
         return tuple(pts)
 
 
+def kernel_path(config: RunConfig) -> str:
+    """The step-kernel family ``ctqw_evolve`` will run for this configuration
+    (the dispatch of csrc/api.cu): "resident", "plane3", "band4", "tile" or
+    "generic"."""
+    lat = config.space.lattice
+    st = config.stepper
+    m, n = config.space.m, lat.n_sites
+    ring = lat.q == 1 and lat.k_half == (1,) and lat.boundary == "periodic" and n >= 3
+    pinned = os.environ.get("CTQW_STREAM", "")
+    order_ok = st.backend == "rk4" or 1 <= st.taylor_order <= 4
+    if not ring or pinned == "generic":
+        return "generic"
+    if m == 2 and n <= 64 and pinned == "" and (st.backend == "rk4" or st.taylor_order <= 16):
+        return "resident"
+    if m == 3 and n == 128 and (st.backend == "rk4" or st.taylor_order == 4) and pinned in ("", "plane3"):
+        return "plane3"
+    if m == 2 and order_ok and n % 4 == 0 and n >= 16 and n // 4 <= 256 and pinned in ("", "band4"):
+        return "band4"
+    if m == 2 and n > 64 and (st.backend == "rk4" or st.taylor_order <= 4) and pinned in ("", "tile", "band4"):
+        return "tile"
+    return "generic"
+
+
+# full state stacks each path keeps on the device (caller's + library's)
+_PATH_BUFFERS = {"resident": 1, "plane3": 1, "band4": 2, "tile": 2, "generic": 4}
+
+
 def estimate_memory(config: RunConfig, world: int = 1) -> dict:
     """Device working set per GPU in bytes (keys of ensemble.py:297-323).
 
-    States are complex128 regardless of ``precision``; the stack and one
-    work buffer of the same size (ping-pong of the streaming path), O(N)
-    coefficients per realization instead of the (D, H+1) value table, no
-    topology table, and the D-double diagonal instead of the packed rho.
+    States are complex128 regardless of ``precision``.  The number of full
+    state stacks follows the kernel path (``kernel_path``): one for the
+    in-place resident and plane3 kernels, two for the ping-pong streaming
+    kernels, four for the generic per-application path (stack, work and two
+    library term buffers).  Plus O(N) coefficients per realization instead of
+    the (D, H+1) value table, the per-realization norm statistics and event
+    buffers, the telegraph process state for dynamic noise, no topology
+    table, and the diagonal (limbs, sum, joint) instead of the packed rho.
     """
     space = config.space
     dim = space.dim
     n = space.lattice.n_sites
     r_local = -(-config.realizations // world)
     state = r_local * dim * 16
-    buffers = 1 if marches_in_place(config) else 2
-    coeff = r_local * n * 8 * (2 + space.lattice.moves_half)
+    path = kernel_path(config)
+    buffers = _PATH_BUFFERS[path]
+    k_links = n * sum(space.lattice.k_half)
+    coeff = r_local * (k_links + n) * 8
+    stats = r_local * (48 + 100 * 16 + 8 + 32 * 8)  # RealStat, EventRec[100], rescale, norm partials
+    noise_state = 0
+    if not config.noise.is_static:
+        total = k_links + n
+        noise_state = r_local * (total * (8 + 8 + 12) + 64)  # values, switch times, due lists, generator
+    density = dim * (24 + 8 + 8)  # int64 limbs, diagonal sum, joint distribution
     return {
         "joint_dim": dim,
         "itemsize": 16,
+        "kernel_path": path,
+        "state_buffers": buffers,
         "state_bytes": buffers * state,
-        "hamiltonian_bytes": coeff,
+        "hamiltonian_bytes": coeff + noise_state,
+        "statistics_bytes": stats,
         "topology_bytes": 0,
-        "density_bytes": dim * 8 * 2,
-        "total_bytes": buffers * state + coeff + dim * 16,
+        "density_bytes": density,
+        "total_bytes": buffers * state + coeff + noise_state + stats + density,
     }
 
 
 def marches_in_place(config: RunConfig) -> bool:
-    """The m = 3, N = 128 cluster kernel updates the states in place (one
-    buffer, so twice the realizations per GPU -- configs[4])."""
-    lat = config.space.lattice
-    st = config.stepper
-    return (config.space.m == 3 and lat.q == 1 and lat.k_half == (1,) and lat.boundary == "periodic"
-            and lat.n_sites == 128 and (st.backend == "rk4" or st.taylor_order == 4)
-            and os.environ.get("CTQW_STREAM", "") in ("", "plane3"))
+    """The resident (m = 2, N <= 64) and m = 3, N = 128 cluster kernels update
+    the states in place: one buffer (so twice the realizations per GPU --
+    configs[4])."""
+    return kernel_path(config) in ("resident", "plane3")
 
 
 class OutputSinks:
@@ -493,7 +532,11 @@ class PendingObservables:
 
     @property
     def participation_ratio(self):
-        return float(self.host()[self.n + 2])
+        h = self.host()
+        s2 = float(h[self.n + 1])
+        if s2 <= 0.0:  # NaN passes through (a blown-up state), as in observables.py:94-101
+            raise NumericError("joint distribution has no weight")
+        return float(h[self.n + 2])
 
     @property
     def purity(self):
