@@ -751,9 +751,12 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       // band4 compiles N in for the four-application steps at the BASELINE sizes
       const int nn = (use_band4 && napp == 4 && (h->n == 256 || h->n == 512 || h->n == 1024)) ? h->n
                      : use_plane3 ? 128 : 0;
-      std::snprintf(h->variant, sizeof(h->variant), "%s<%s,napp=%d,site=%d,exact=%d,NN=%d>", h->stream_kernel,
+      // band4's zero-diagonal form (eps0 = U = 0) at the compile-time sizes
+      const bool zd = h->k.base[0] == 0.0 && h->k.base[1] == 0.0 && h->k.base[2] == 0.0 && h->k.base[3] == 0.0;
+      const int dg = (use_band4 && nn > 0 && zd) ? 0 : 2;
+      std::snprintf(h->variant, sizeof(h->variant), "%s<%s,napp=%d,site=%d,exact=%d,NN=%d,dg=%d>", h->stream_kernel,
                     sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", napp, coef.site != nullptr ? 1 : 0,
-                    exact ? 1 : 0, nn);
+                    exact ? 1 : 0, nn, dg);
     }
     const int nparts = use_plane3 ? plane3_parts()
                        : use_band4 ? band4_parts(h->n)

@@ -155,6 +155,10 @@ __device__ __forceinline__ void fixed_split(double x, long long& l2, long long& 
   l0 = __double2ll_rn(__dmul_rn(a0, 0x1p110));
 }
 
+// |z|^2 = re*re + im*im, each product rounded (no FMA contraction), as NumPy
+// forms it: the term -- and so its limbs -- is a pure function of z.
+__device__ __forceinline__ double norm2_rn(double2 z) { return __dadd_rn(__dmul_rn(z.x, z.x), __dmul_rn(z.y, z.y)); }
+
 // acc[k][alpha] += sum_{r in this block's realization range} limb_k(|psi_r(alpha)|^2)
 __global__ void observe_diag_fixed_kernel(const double2* __restrict__ psi, int64_t count, int64_t dim,
                                           int64_t rspan, unsigned long long* __restrict__ acc) {
@@ -167,7 +171,7 @@ __global__ void observe_diag_fixed_kernel(const double2* __restrict__ psi, int64
   for (; r + 4 <= r1; r += 4) {
     double v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = norm2(__ldg(psi + (r + u) * dim + a));
+    for (int u = 0; u < 4; ++u) v[u] = norm2_rn(__ldg(psi + (r + u) * dim + a));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       long long l2, l1, l0;
@@ -179,7 +183,7 @@ __global__ void observe_diag_fixed_kernel(const double2* __restrict__ psi, int64
   }
   for (; r < r1; ++r) {
     long long l2, l1, l0;
-    fixed_split(norm2(__ldg(psi + r * dim + a)), l2, l1, l0);
+    fixed_split(norm2_rn(__ldg(psi + r * dim + a)), l2, l1, l0);
     s2 += l2;
     s1 += l1;
     s0 += l0;

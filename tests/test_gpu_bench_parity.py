@@ -69,7 +69,7 @@ def test_band4_bench_variants_match_oracle(pkg, case):
     n, B, backend, dt, steps, target, rescale = case
     h, st, _keep = device_case(2, n, B, target, onsite=0.0, U=0.0)
     site = int(target in ("onsite", "both"))
-    var = "band4_kernel<{},napp=4,site={},exact={},NN={}>"
+    var = "band4_kernel<{},napp=4,site={},exact={},NN={},dg=0>"
     _check(h, st, 2, n, B, backend, dt, steps, var.format(backend, site, 1, n), var.format(backend, site, 0, n),
            rescale)
 
@@ -87,7 +87,7 @@ def test_plane3_bench_variants_match_oracle(pkg, case):
     B, backend, dt, steps, target, rescale = case
     h, st, _keep = device_case(3, 128, B, target, onsite=0.0, U=0.0)
     site = int(target in ("onsite", "both"))
-    var = "plane3_kernel<{},napp=4,site={},exact={},NN=128>"
+    var = "plane3_kernel<{},napp=4,site={},exact={},NN=128,dg=2>"
     _check(h, st, 3, 128, B, backend, dt, steps, var.format(backend, site, 1), var.format(backend, site, 0),
            rescale)
 
