@@ -793,4 +793,4 @@ def test_observe_diag_fixed_limbs_bitwise(pkg):
         d2 = torch.empty_like(diag)
         h.observe_diag(dev, R, d2)
         np.testing.assert_array_equal(d2.cpu().numpy(), diag.cpu().numpy())
-        np.testing.assert_allclose(diag.cpu().numpy(), (np.abs(psi) ** 2).sum(axis=0), rtol=1e-15)
+        np.testing.assert_allclose(diag.cpu().numpy(), (np.abs(psi) ** 2).sum(axis=0), rtol=1e-14)
