@@ -33,6 +33,7 @@ Line printed by rank 0 (one JSON object):
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import socket
@@ -632,12 +633,24 @@ def ours(a):
         # allocator then serves this run's buffers from its cache
         warm = make_config(p, a, R_total, max(a.warmup, 1), local)
         p.run(warm, p.MemorySinks(keep_densities=False), group=group)
+        gc.collect()
         torch.cuda.synchronize()
         barrier()
+        prof = None
+        if os.environ.get("CTQW_E2E_PROFILE"):
+            import cProfile
+
+            prof = cProfile.Profile()
+            prof.enable()
         t0 = time.perf_counter()
         rep = p.run(cfg, sinks, group=group)
         torch.cuda.synchronize()
         e2e_s = all_max(time.perf_counter() - t0)
+        if prof is not None:
+            import pstats
+
+            prof.disable()
+            pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(12)
         n_points = len(cfg.schedule)
         h2d = dim * 16 + 16  # initial state + noise levels
         d2h = (a.n + 4) * 8 * n_points + 48 * n_points  # observable rows + segment statistics per point

@@ -462,6 +462,13 @@ class EnsembleState:
     def states(self):
         return self.psi[: self.count]
 
+    def release(self):
+        """Give the state buffers and the handle back now (not whenever the
+        garbage collector gets to this object): a following run() then
+        reuses the memory instead of mapping fresh tens of GiB."""
+        self.psi = self.work = self.psi0 = self.hop = self.site = None
+        self.handle.close()
+
 
 def _observable_rows(config, pops, pr, purity, joint):
     rows = []
@@ -658,6 +665,7 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
                     emit(sinks.message,
                          f"aborted: norm deviation {dev:.3e} at realization {real}, step {step}; "
                          f"reduce the time step")
+                    ens.release()
                     raise NormFailureError(dev, realization=real, step=step)
                 corrections += merged["corrections"]
                 event_total += merged["event_count"]
@@ -686,6 +694,7 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
 
     with torch.cuda.device(device):
         switches = sharding.allreduce_int_([ens.switch_count()], group)[0]
+        ens.release()
     report = RunReport(config=config, profile=profile, io_seconds=io_seconds,
                        wall_seconds=clock() - wall_start, workers=world, snapshots=snapshots,
                        max_norm_deviation=max_deviation, norm_corrections=corrections,
