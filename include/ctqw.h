@@ -232,6 +232,16 @@ int ctqw_observe_reduce(ctqw_handle_t h, const double *diag_sum_dev, double tota
 int ctqw_overlap_sumsq(ctqw_handle_t h, const double *a_dev, int64_t count_a,
                        const double *b_dev, int64_t count_b, double *sumsq_dev, void *stream);
 
+/* Packed ensemble density matrix (replaces the Gram product of
+ * ctqw/density.py:91-95, accumulate_density): packed_dev[i(i+1)/2 + j] =
+ * scale * sum_r psi_r[i] conj(psi_r[j]) for j <= i, psi_dev an (R, dim)
+ * complex128 stack (interleaved doubles), packed_dev dim(dim+1)/2 complex128.
+ * The reference divides by R (scale = 1/R); scale = 1 gives the raw sums
+ * (multi-GPU: all-reduce, then scale).  Realizations are summed in stack
+ * order.  Needs no model handle; errors go to ctqw_last_error(NULL). */
+int ctqw_packed_gram(const double *psi_dev, int64_t count, int64_t dim, double scale, double *packed_dev,
+                     int32_t device, void *stream);
+
 /* Kernel launches issued by this handle since creation (for bench.py). */
 int64_t ctqw_launch_count(ctqw_handle_t h);
 

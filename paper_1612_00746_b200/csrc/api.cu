@@ -955,6 +955,17 @@ int ctqw_overlap_sumsq(ctqw_handle_t h, const double* a_dev, int64_t count_a, co
   return CTQW_OK;
 }
 
+int ctqw_packed_gram(const double* psi_dev, int64_t count, int64_t dim, double scale, double* packed_dev,
+                     int32_t device, void* stream) {
+  if (count <= 0) return fail_with(nullptr, CTQW_ERR_CONFIG, "empty state stack");
+  if (dim <= 0) return fail_with(nullptr, CTQW_ERR_CONFIG, "dimension must be positive");
+  if (!psi_dev || !packed_dev) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL buffer");
+  DeviceGuard g(device);
+  CUDA_TRY(nullptr, launch_packed_gram((const double2*)psi_dev, count, dim, scale, (double2*)packed_dev,
+                                       (cudaStream_t)stream));
+  return CTQW_OK;
+}
+
 int64_t ctqw_launch_count(ctqw_handle_t h) { return h ? (int64_t)h->launches.load() : 0; }
 
 int ctqw_kernel_timing(ctqw_handle_t h, int32_t enable) {

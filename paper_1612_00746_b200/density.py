@@ -8,15 +8,17 @@ and divides by R.  The hot path only needs diag(rho) (``observables.py``:
 sinks that want it:
 
 * ``accumulate_density(states, time_tag)`` -- the reference's function, on
-  the GPU: the Gram product is one complex128 GEMM (cuBLAS through torch --
-  a plain library GEMM), the triangle is gathered on the device, and the
-  packed vector reaches the host only when ``DensityMatrix.packed`` is read;
+  the GPU: the Gram product runs in a hand-written triangle-only kernel
+  (``csrc/density_gram.cu``, HERK-style: half the multiply-adds of the
+  reference's full GEMM, no D x D transient) that writes the packed lower
+  triangle directly; it reaches the host only when ``DensityMatrix.packed``
+  is read;
 * ``run`` computes it at every collection point for sinks whose
   ``dense_density`` attribute is true (``MemorySinks(dense=True)``), within
   the reference's own size limit (the D x D transient).
 
 Results equal the reference's to rounding (BLAS summation order), checked to
-1e-12 against its own output in ``tests/test_gpu_parity.py``.
+1e-15 against its own output in ``tests/test_gpu_parity.py``.
 """
 
 from __future__ import annotations
@@ -80,26 +82,21 @@ class DensityMatrix:
         return float(2.0 * np.sum(np.abs(p) ** 2) - np.sum(np.abs(d) ** 2))
 
 
-def _tril_index(dim: int, device):
+def packed_density_device(stack_dev, count: int, scale: float | None = None):
+    """Packed scale * lower(stack^T conj(stack)) of a device (R, D) complex128
+    stack (density.py:91-96; default scale 1/R, NumPy's ``packed /= r``
+    multiplies by the reciprocal), by ``ctqw_packed_gram``."""
     import torch
 
-    rows, cols = torch.tril_indices(dim, dim, device=device)
-    return rows * dim + cols
-
-
-def packed_density_device(stack_dev, count: int):
-    """Packed (1/R) * lower(stack^T conj(stack)) of a device (R, D) complex128
-    stack, on the device (density.py:91-96)."""
-    import torch
+    from . import native
 
     dim = stack_dev.shape[1]
     if dim > DENSE_DIM_CAP:
         raise CapacityError(f"dense density of dimension {dim} exceeds the cap {DENSE_DIM_CAP}")
-    s = stack_dev[:count]
-    gram = s.transpose(0, 1) @ s.conj()          # (D, D): sum_r psi_r[i] conj(psi_r[j])
-    packed = gram.reshape(-1)[_tril_index(dim, s.device)]
-    del gram
-    return packed / count
+    s = stack_dev[:count].contiguous()
+    packed = torch.empty(packed_length(dim), dtype=torch.complex128, device=s.device)
+    native.packed_gram(s, count, packed, 1.0 / count if scale is None else scale)
+    return packed
 
 
 def accumulate_density(states, time_tag: float | None = None) -> DensityMatrix:

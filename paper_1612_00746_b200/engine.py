@@ -498,7 +498,7 @@ def _dense_snapshot(config, ens, group, time_tag):
 
     dim = config.space.dim
     if ens.count:
-        part = packed_density_device(ens.states(), ens.count) * ens.count
+        part = packed_density_device(ens.states(), ens.count, scale=1.0)
     else:
         part = torch.zeros(packed_length(dim), dtype=torch.complex128, device=ens.dev)
     if group is not None and sharding._collective(group):
@@ -508,7 +508,7 @@ def _dense_snapshot(config, ens, group, time_tag):
         dist.all_reduce(real, group=group)
         part = torch.view_as_complex(real)
     return DensityMatrix(None, dim=dim, sample_count=config.realizations, time_tag=float(time_tag),
-                         device_packed=part / config.realizations)
+                         device_packed=part * (1.0 / config.realizations))
 
 
 class PendingObservables:

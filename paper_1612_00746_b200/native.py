@@ -107,6 +107,7 @@ SIGNATURES = {
     "ctqw_fixed_to_double": (ctypes.c_int, [_P, _P, _P, _P]),
     "ctqw_observe_reduce": (ctypes.c_int, [_P, _P, _D, _P, _P, _P, _P]),
     "ctqw_overlap_sumsq": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
+    "ctqw_packed_gram": (ctypes.c_int, [_P, _I64, _I64, _D, _P, _I32, _P]),
     "ctqw_launch_count": (ctypes.c_int64, [_P]),
     "ctqw_kernel_timing": (ctypes.c_int, [_P, _I32]),
     "ctqw_kernel_time": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
@@ -361,6 +362,16 @@ class Handle:
                                                 int(count_b), _ptr(out), self.stream))
 
 
+def packed_gram(stack, count: int, packed, scale: float):
+    """packed[i(i+1)/2 + j] = scale * sum_r stack[r, i] conj(stack[r, j]), j <= i
+    (hand-written triangle-only kernel; density.py:91-95)."""
+    lib = load_library()
+    dev = stack.device.index
+    code = lib.ctqw_packed_gram(_ptr(stack), int(count), int(stack.shape[1]), float(scale), _ptr(packed),
+                                int(dev), _stream(dev))
+    _raise_for(code, None)
+
+
 def exported_symbols(path: str | None = None) -> list[str]:
     """Names of the C-ABI entry points the library exports (CPU-safe check)."""
     lib = load_library(path)
@@ -368,4 +379,4 @@ def exported_symbols(path: str | None = None) -> list[str]:
 
 
 __all__ = ["Handle", "Model", "Stepper", "SegmentStats", "load_library", "exported_symbols",
-           "make_stepper", "CtqwError", "LIB_PATH", "SIGNATURES"]
+           "make_stepper", "packed_gram", "CtqwError", "LIB_PATH", "SIGNATURES"]

@@ -658,6 +658,37 @@ def test_run_dense_snapshots_match_reference(pkg):
                                                - np.sum(np.abs(np.diagonal(d.dense())) ** 2)), rel=1e-12)
 
 
+@pytest.mark.parametrize("dim,R", [(1, 1), (1, 5), (63, 17), (64, 16), (65, 33), (200, 1), (300, 100)])
+def test_packed_gram_kernel_matches_numpy(pkg, dim, R):
+    """ctqw_packed_gram (the triangle-only kernel) against the reference's
+    formula gram = stack.T @ stack.conj(); packed = gram[tril] * (1/R)
+    (density.py:91-95), on ragged sizes (tile edges, a single realization,
+    R not a multiple of the staging depth)."""
+    from paper_1612_00746_b200 import density, native
+
+    rng = np.random.default_rng(dim * 1000 + R)
+    stack = rng.standard_normal((R, dim)) + 1j * rng.standard_normal((R, dim))
+    dev = torch.as_tensor(stack, device="cuda:0")
+    got = density.packed_density_device(dev, R).cpu().numpy()
+    gram = stack.T @ stack.conj()
+    rows, cols = np.tril_indices(dim)
+    ref = gram[rows, cols] * (1.0 / R)
+    scale = np.abs(ref).max()
+    assert np.abs(got - ref).max() <= 1e-14 * scale * max(1, R / 10)
+    raw = torch.empty(dim * (dim + 1) // 2, dtype=torch.complex128, device="cuda:0")
+    native.packed_gram(dev, R, raw, 1.0)
+    assert np.abs(raw.cpu().numpy() - gram[rows, cols]).max() <= 1e-14 * R * scale * max(1, R / 10)
+
+
+def test_packed_gram_rejects_empty_stack(pkg):
+    from paper_1612_00746_b200 import native
+
+    dev = torch.zeros((1, 8), dtype=torch.complex128, device="cuda:0")
+    out = torch.empty(36, dtype=torch.complex128, device="cuda:0")
+    with pytest.raises(pkg.ConfigurationError):
+        native.packed_gram(dev, 0, out, 1.0)
+
+
 # ---------------------------------------------------------------------------
 # general lattices (q > 1, k_half > 1, open boundaries): generic kernels
 
