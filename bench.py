@@ -584,7 +584,7 @@ def ours(a):
     h.kernel_timing(False)
     launches = h.launches - launches0
     assert stats["failure"] is None
-    assert abs(pend.populations.sum() - a.m) < 1e-6
+    assert abs(pend.populations.sum() - a.m) < 4 * a.m * 1e-6  # within the norm policy tol_norm
 
     ms_other = None
     if not a.no_other:
@@ -601,7 +601,7 @@ def ours(a):
     # roofline of the dominant kernel (streaming step / resident segment)
     avg_launch_ms = kernel_ms / max(kernel_launches, 1)
     steps_per_launch = 1
-    if kernel == "resident_kernel":
+    if kernel.startswith("resident"):
         steps_per_launch = a.steps // max(kernel_launches, 1)  # one launch covers a whole segment
     bytes_per_launch = (hi - lo) * 32.0 * dim * steps_per_launch
     achieved = bytes_per_launch / (avg_launch_ms / 1000.0) / 1e9

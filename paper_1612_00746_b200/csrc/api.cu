@@ -701,16 +701,23 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   // a pinned streaming family (CTQW_STREAM) bypasses the resident path;
   // general lattices (move tables) run on the generic kernels only
   if (h->stream_kind == 0 && !h->general && resident_supported(h->m, h->n, sc)) {
-    h->stream_kernel = "resident_kernel";
-    std::snprintf(h->variant, sizeof(h->variant), "resident_kernel<%s,order=%d,site=%d,exact=%d,N=%d>",
+    // N = 64 with <= 4 applications per step: the 4 x 4-block kernel
+    // (resident64.cu); other sizes / orders: the column-strip kernel
+    const bool r64 = resident64_supported(h->m, h->n, sc) && !std::getenv("CTQW_RESIDENT_STRIP");
+    h->stream_kernel = r64 ? "resident64_kernel" : "resident_kernel";
+    std::snprintf(h->variant, sizeof(h->variant), "%s<%s,order=%d,site=%d,exact=%d,N=%d>", h->stream_kernel,
                   sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", sc.order, coef.site != nullptr ? 1 : 0,
                   exact ? 1 : 0, h->n);
     // dynamic noise changes the couplings after every step: one step per launch
     const int64_t chunk = h->tg_enabled ? 1 : n_steps;
     for (int64_t j = 0; j < n_steps; j += chunk) {
       timing_event(h, s);
-      CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step + j, chunk,
-                                  h->stats, h->events, h->fail, s));
+      if (r64)
+        CUDA_TRY(h, launch_resident64(psi, count, coef, h->k, sc, exact, pol, first_step + j, chunk, h->stats,
+                                      h->events, h->fail, s));
+      else
+        CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step + j, chunk,
+                                    h->stats, h->events, h->fail, s));
       timing_event(h, s);
       h->timed_launches += h->timing ? 1 : 0;
       h->launches += 1;

@@ -100,6 +100,11 @@ struct TileGeom {
 };
 bool tile_supported(int m, int n, const StepScalars& sc);
 bool resident_supported(int m, int n, const StepScalars& sc);
+bool resident64_supported(int m, int n, const StepScalars& sc);
+cudaError_t launch_resident64(double2* psi, int64_t count, const Coef& coef, const StencilConst& k,
+                              const StepScalars& sc, bool exact, const NormPolicy& pol, long long first_step,
+                              long long n_steps, RealStat* stats, EventRec* events, long long* fail,
+                              cudaStream_t s);
 int tile_parts(int n, const StepScalars& sc);
 cudaError_t launch_tile_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
                              const Coef& coef, const StencilConst& k, const StepScalars& sc,

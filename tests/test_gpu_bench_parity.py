@@ -99,10 +99,10 @@ def test_resident_config0_variant_matches_oracle(pkg):
     psi0 = np.tile(orc.product_state(2, n), (B, 1))
     ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, "taylor", 4)
     mine, _ = run_evolve(h, psi0, B, steps, stepper("taylor", 4, dt, exact=True))
-    assert h.step_variant() == "resident_kernel<taylor,order=4,site=0,exact=1,N=64>"
+    assert h.step_variant() == "resident64_kernel<taylor,order=4,site=0,exact=1,N=64>"
     np.testing.assert_array_equal(mine, ref)
     fma, _ = run_evolve(h, psi0, B, steps, stepper("taylor", 4, dt, exact=False))
-    assert h.step_variant() == "resident_kernel<taylor,order=4,site=0,exact=0,N=64>"
+    assert h.step_variant() == "resident64_kernel<taylor,order=4,site=0,exact=0,N=64>"
     assert np.abs(fma - ref).max() <= 1e-12
 
 
@@ -127,3 +127,50 @@ def test_run_config0_full_length_matches_reference(pkg, exact):
     np.testing.assert_allclose(mine, data["rows"], rtol=1e-10, atol=1e-13)
     assert report.norm_corrections == meta["corrections"]
     assert report.snapshots == 150
+
+
+RESIDENT64 = [
+    # (B, backend, order, dt, steps, target, onsite, U, expect_rescale): every
+    # template branch of resident64_kernel (zero / uniform / coincidence
+    # diagonal, site noise, Taylor orders 1-4, RK4, rescales)
+    (7, "taylor", 4, 0.02, 30, "tunneling", 0.0, 0.0, False),
+    (7, "taylor", 4, 0.12, 12, "tunneling", 0.0, 0.0, True),
+    (5, "taylor", 4, 0.02, 20, "both", 0.2, 0.7, False),
+    (5, "taylor", 3, 0.02, 20, "both", 0.2, 0.7, True),
+    (5, "taylor", 2, 0.01, 20, "onsite", 0.1, 0.0, True),
+    (5, "taylor", 1, 0.002, 10, "both", 0.0, 0.5, True),
+    (5, "rk4", 4, 0.02, 25, "both", 0.2, 0.7, False),
+    (5, "rk4", 4, 0.12, 10, "tunneling", 0.0, 0.0, True),
+    (3, "taylor", 4, 0.1, 15, "both", 0.3, 1.1, True),
+]
+
+
+@pytest.mark.parametrize("case", RESIDENT64, ids=[f"B{c[0]}{c[1]}{c[2]}dt{c[3]}{c[5]}U{c[7]}" for c in RESIDENT64])
+def test_resident64_variants_match_oracle(pkg, case):
+    B, backend, order, dt, steps, target, onsite, U, rescale = case
+    h, st, _keep = device_case(2, 64, B, target, onsite=onsite, U=U)
+    psi0 = np.tile(orc.product_state(2, 64), (B, 1))
+    ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, order)
+    assert (ostats.corrections > 0) == rescale
+    site = int(target in ("onsite", "both"))
+    for exact in (True, False):
+        mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, order, dt, exact=exact))
+        assert h.step_variant() == f"resident64_kernel<{backend},order={order},site={site},exact={int(exact)},N=64>"
+        assert stats.corrections == ostats.corrections and stats.event_count == ostats.event_count
+        if exact and ostats.event_count == 0:
+            np.testing.assert_array_equal(mine, ref)
+        else:
+            assert np.abs(mine - ref).max() <= (1e-13 if exact else 1e-12)
+
+
+def test_resident64_equals_strip_kernel(pkg, monkeypatch):
+    """The 4 x 4-block kernel and the column-strip kernel (CTQW_RESIDENT_STRIP)
+    give the same bits in exact mode (same operation order per amplitude)."""
+    B, dt, steps = 4, 0.03, 25
+    h, st, _keep = device_case(2, 64, B, "both", onsite=0.2, U=0.7)
+    psi0 = np.tile(orc.product_state(2, 64), (B, 1))
+    a, _ = run_evolve(h, psi0, B, steps, stepper("taylor", 4, dt, exact=True))
+    monkeypatch.setenv("CTQW_RESIDENT_STRIP", "1")
+    b, _ = run_evolve(h, psi0, B, steps, stepper("taylor", 4, dt, exact=True))
+    assert h.step_variant().startswith("resident_kernel<")
+    np.testing.assert_array_equal(a, b)
