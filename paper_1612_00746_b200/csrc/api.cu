@@ -760,7 +760,8 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
                      : use_plane3 ? 128 : 0;
       // band4's zero-diagonal form (eps0 = U = 0) at the compile-time sizes
       const bool zd = h->k.base[0] == 0.0 && h->k.base[1] == 0.0 && h->k.base[2] == 0.0 && h->k.base[3] == 0.0;
-      const int dg = (use_band4 && nn > 0 && zd) ? 0 : 2;
+      // (plane3: without site noise)
+      const int dg = ((use_band4 && nn > 0 && zd) || (use_plane3 && zd && coef.site == nullptr)) ? 0 : 2;
       std::snprintf(h->variant, sizeof(h->variant), "%s<%s,napp=%d,site=%d,exact=%d,NN=%d,dg=%d>", h->stream_kernel,
                     sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", napp, coef.site != nullptr ? 1 : 0,
                     exact ? 1 : 0, nn, dg);

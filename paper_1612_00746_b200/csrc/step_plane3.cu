@@ -283,7 +283,7 @@ __device__ __forceinline__ void xch_put(const T3& T, int k, int buf, const Quad&
 // (H z) on the block at plane r: up / mid / dn = planes r-1, r, r+1.
 // out = i*ci*(H z), or with HORN psi + i*ci*(H z) (Horner-form Taylor, as
 // step_band4.cu).
-template <bool EXACT, bool SITE, bool HORN = false, bool RAW = false>
+template <bool EXACT, bool SITE, bool HORN = false, bool RAW = false, bool ZD = false>
 __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
                                        const Quad& dn, const Nb& nb, double ci, Quad& out,
                                        const Quad* psi = nullptr) {
@@ -304,16 +304,24 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
   for (int q = 0; q < 4; ++q) {
     const int a = q >> 1, b = q & 1;
     const int x1 = T.x1a + a, x2 = T.x2a + b;
-    const int cc = (r == x1) + (r == x2) + (x1 == x2);
-    double v0 = K.base[cc];
-    if (SITE) v0 = __dadd_rn(v0, __dadd_rn(__dadd_rn(s0, s1[a]), s2[b]));
     const double2 x1p = a == 1 ? nb.x1p[b] : mid.c[2 + b];
     const double2 x1m = a == 0 ? nb.x1m[b] : mid.c[b];
     const double2 x2p = b == 1 ? nb.x2p[a] : mid.c[2 * a + 1];
     const double2 x2m = b == 0 ? nb.x2m[a] : mid.c[2 * a];
-    double2 h = rmul(v0, mid.c[q]);
-    if (EXACT) h = madd<EXACT>(h, h0.y, dn.c[q]);  // particle 0 +move (plane r+1), hop[x0]
-    h = madd<EXACT>(h, h0.x, up.c[q]);        // particle 0 -move (plane r-1), hop[x0-1]
+    double2 h;
+    if constexpr (ZD) {
+      // eps0 = U = 0, no site noise: the diagonal is zero, the sum starts at
+      // the first neighbour product (0 + x == x: the reference's bits)
+      if (EXACT) h = madd<EXACT>(rmul(h0.y, dn.c[q]), h0.x, up.c[q]);
+      else h = rmul(h0.x, up.c[q]);
+    } else {
+      const int cc = (r == x1) + (r == x2) + (x1 == x2);
+      double v0 = K.base[cc];
+      if (SITE) v0 = __dadd_rn(v0, __dadd_rn(__dadd_rn(s0, s1[a]), s2[b]));
+      h = rmul(v0, mid.c[q]);
+      if (EXACT) h = madd<EXACT>(h, h0.y, dn.c[q]);  // particle 0 +move (plane r+1), hop[x0]
+      h = madd<EXACT>(h, h0.x, up.c[q]);        // particle 0 -move (plane r-1), hop[x0-1]
+    }
     h = madd<EXACT>(h, h1[1 + a], x1p);     // particle 1 +move, hop[x1]
     h = madd<EXACT>(h, h1[a], x1m);         // particle 1 -move, hop[x1-1]
     h = madd<EXACT>(h, h2[1 + b], x2p);     // particle 2 +move, hop[x2]
@@ -430,7 +438,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 // Stage K (2..NAPP) of iteration j: plane j-K+1 from (old, mid, dn) =
 // stage K-1's planes j-K, j-K+1, j-K+2 and the in-plane neighbours of the
 // middle one.  Returns the stage's output (the next stage's dn).
-template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH, int K>
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD, bool SC, int PH, int K>
 __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i,
                                              int j, const Quad& mid, const Quad& dn, const Nb& nb) {
   constexpr double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
@@ -443,7 +451,7 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
   constexpr bool RKF = RK4 && !EXACT && !SITE;
   const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[NAPP - K] : a.ci[K - 1]);
   Quad tk;
-  apply3<EXACT, SITE, HORN, RKF>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk, &R.acc[s0]);
+  apply3<EXACT, SITE, HORN, RKF, ZD>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk, &R.acc[s0]);
   R.old[K - 1] = mid;
   Quad nk;
   if constexpr (RKF) {
@@ -492,7 +500,7 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
   return nk;
 }
 
-template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int PH>
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD, bool SC, int PH>
 __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i) {
   const int j = P.j0 + i;
   wait_plane(P, i + 2);
@@ -525,7 +533,7 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   constexpr bool HORN = !RK4 && !EXACT;
   constexpr bool RKF = RK4 && !EXACT && !SITE;
   Quad t;
-  apply3<EXACT, SITE, HORN, RKF>(T, a.k, r, R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
+  apply3<EXACT, SITE, HORN, RKF, ZD>(T, a.k, r, R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
   const Quad mid1 = R.m1;  // t1 (arg1) of plane j-1
   Quad nt;
   if constexpr (RKF) {
@@ -553,29 +561,29 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   if (i < P.iters - 1) halo_push(T, 0, buf, nt);
   R.m1 = nt;
   halo_wait(T, 0, i);
-  const Quad t2 = plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
+  const Quad t2 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
   halo_wait(T, 1, i);
-  const Quad t3 = plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, 3>(a, T, P, R, i, j, xch_own(T, 1, buf ^ 1), t2,
+  const Quad t3 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 3>(a, T, P, R, i, j, xch_own(T, 1, buf ^ 1), t2,
                                                                   xch_nb(T, 1, buf ^ 1));
   halo_wait(T, 2, i);
-  plane3_stage<NAPP, RK4, SITE, EXACT, SC, PH, NAPP>(a, T, P, R, i, j, xch_own(T, NAPP - 2, buf ^ 1), t3,
+  plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, NAPP>(a, T, P, R, i, j, xch_own(T, NAPP - 2, buf ^ 1), t3,
                                                      xch_nb(T, NAPP - 2, buf ^ 1));
   if (RK4) R.acc[PH] = t;
   cluster_arrive();
 }
 
-template <int NAPP, bool RK4, bool SITE, bool EXACT, bool SC>
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD, bool SC>
 __device__ __forceinline__ void plane3_loop(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R,
                                             int iters) {
 #pragma unroll 1
   for (int i = 0; i < iters; i += 3) {
-    plane3_iter<NAPP, RK4, SITE, EXACT, SC, 0>(a, T, P, R, i);
-    plane3_iter<NAPP, RK4, SITE, EXACT, SC, 1>(a, T, P, R, i + 1);
-    plane3_iter<NAPP, RK4, SITE, EXACT, SC, 2>(a, T, P, R, i + 2);
+    plane3_iter<NAPP, RK4, SITE, EXACT, ZD, SC, 0>(a, T, P, R, i);
+    plane3_iter<NAPP, RK4, SITE, EXACT, ZD, SC, 1>(a, T, P, R, i + 1);
+    plane3_iter<NAPP, RK4, SITE, EXACT, ZD, SC, 2>(a, T, P, R, i + 2);
   }
 }
 
-template <int NAPP, bool RK4, bool SITE, bool EXACT>
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD>
 __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_constant__ Plane3Args a) {
   static_assert(NAPP == 4, "plane3 pipelines four applications (Taylor-4 / RK4)");
   cg::cluster_group cluster = cg::this_cluster();
@@ -667,7 +675,7 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
 #pragma unroll
       for (int q = 0; q < 4; ++q) R.acc[w].c[q] = make_double2(0.0, 0.0);
     R.nrm = 0.0;
-    plane3_loop<NAPP, RK4, SITE, EXACT, false>(a, T, P, R, iters);  // ring tiles arrive pre-scaled
+    plane3_loop<NAPP, RK4, SITE, EXACT, ZD, false>(a, T, P, R, iters);  // ring tiles arrive pre-scaled
     cluster_wait();   // completes the last iteration's arrive
     __syncthreads();  // the last stage has written its norm partials
     flush3(T, P, true);
@@ -748,9 +756,9 @@ double2* side_buffer(int nclus) {
   return buf[dev];
 }
 
-template <int NAPP, bool RK4, bool SITE, bool EXACT>
+template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD>
 cudaError_t launch_p3(Plane3Args a, const double2* psi_in, cudaStream_t s) {
-  auto kern = plane3_kernel<NAPP, RK4, SITE, EXACT>;
+  auto kern = plane3_kernel<NAPP, RK4, SITE, EXACT, ZD>;
   static int nclus_dev[64] = {};
   int& nclus = nclus_dev[current_device() & 63];
   if (nclus == 0) {
@@ -827,16 +835,20 @@ cudaError_t launch_plane3_step(const double2* psi_in, double2* psi_out, int64_t 
   a.fail = fail;
   const bool site = coef.site != nullptr;
   const bool rk4 = sc.backend == 1;
-#ifdef P3_ONLY  // register-pressure experiments: one instantiation
-  return launch_p3<4, false, false, false>(a, psi_in, s);
-#else
+  // eps0 = U = 0 and no site noise (configs[4]): zero diagonal
+  const bool zd = !site && k.base[0] == 0.0 && k.base[1] == 0.0 && k.base[2] == 0.0 && k.base[3] == 0.0;
   if (rk4) {
-    if (site) return exact ? launch_p3<4, true, true, true>(a, psi_in, s) : launch_p3<4, true, true, false>(a, psi_in, s);
-    return exact ? launch_p3<4, true, false, true>(a, psi_in, s) : launch_p3<4, true, false, false>(a, psi_in, s);
+    if (site) return exact ? launch_p3<4, true, true, true, false>(a, psi_in, s)
+                           : launch_p3<4, true, true, false, false>(a, psi_in, s);
+    if (zd) return exact ? launch_p3<4, true, false, true, true>(a, psi_in, s)
+                         : launch_p3<4, true, false, false, true>(a, psi_in, s);
+    return exact ? launch_p3<4, true, false, true, false>(a, psi_in, s) : launch_p3<4, true, false, false, false>(a, psi_in, s);
   }
-  if (site) return exact ? launch_p3<4, false, true, true>(a, psi_in, s) : launch_p3<4, false, true, false>(a, psi_in, s);
-  return exact ? launch_p3<4, false, false, true>(a, psi_in, s) : launch_p3<4, false, false, false>(a, psi_in, s);
-#endif
+  if (site) return exact ? launch_p3<4, false, true, true, false>(a, psi_in, s)
+                         : launch_p3<4, false, true, false, false>(a, psi_in, s);
+  if (zd) return exact ? launch_p3<4, false, false, true, true>(a, psi_in, s)
+                       : launch_p3<4, false, false, false, true>(a, psi_in, s);
+  return exact ? launch_p3<4, false, false, true, false>(a, psi_in, s) : launch_p3<4, false, false, false, false>(a, psi_in, s);
 }
 
 }  // namespace ctqw

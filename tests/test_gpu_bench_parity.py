@@ -87,8 +87,9 @@ def test_plane3_bench_variants_match_oracle(pkg, case):
     B, backend, dt, steps, target, rescale = case
     h, st, _keep = device_case(3, 128, B, target, onsite=0.0, U=0.0)
     site = int(target in ("onsite", "both"))
-    var = "plane3_kernel<{},napp=4,site={},exact={},NN=128,dg=2>"
-    _check(h, st, 3, 128, B, backend, dt, steps, var.format(backend, site, 1), var.format(backend, site, 0),
+    var = "plane3_kernel<{},napp=4,site={},exact={},NN=128,dg={}>"
+    dg = 2 if site else 0  # zero-diagonal form when eps0 = U = 0 and no site noise
+    _check(h, st, 3, 128, B, backend, dt, steps, var.format(backend, site, 1, dg), var.format(backend, site, 0, dg),
            rescale)
 
 
