@@ -242,6 +242,39 @@ int ctqw_overlap_sumsq(ctqw_handle_t h, const double *a_dev, int64_t count_a,
 int ctqw_packed_gram(const double *psi_dev, int64_t count, int64_t dim, double scale, double *packed_dev,
                      int32_t device, void *stream);
 
+/* ctqw_evolve plus the collection points of the schedule, in one call
+ * (replaces the _evolve_segment + accumulate_density-diagonal pairs of
+ * ensemble.py:722-769 for a run of segments).  Every step g =
+ * first_step + k * post_rate (k >= 1) up to first_step + n_steps, and the
+ * last one, is a collection point; point idx = ceil((g - first_step) /
+ * post_rate) - 1 (ceil(n_steps / post_rate) points) receives the exact int64
+ * limbs of sum_r |psi_r(g)|^2 in acc_dev[idx][3][dim] (zeroed by the call; same limbs
+ * as ctqw_observe_diag_fixed).  On the resident N = 64 path the sum is
+ * fused into the step kernel; elsewhere each segment is followed by the
+ * limb pass.  Statistics accumulate over the whole call (ctqw_segment_stats,
+ * ctqw_segment_events).  n_steps >= 1, post_rate >= 1. */
+int ctqw_evolve_observe(ctqw_handle_t h, double *psi_dev, double *work_dev, int64_t count, int64_t first_step,
+                        int64_t n_steps, int64_t post_rate, int64_t *acc_dev, const ctqw_stepper_t *stepper,
+                        int32_t *result_in_work, void *stream);
+
+/* The events of the last evolve / evolve_observe call with step in
+ * (step_lo, step_hi], first CTQW_MAX_EVENTS in (step, realization) order
+ * (one segment's list, as _evolve_segment reports it); event_count = events
+ * in that range still held in the per-realization logs (CTQW_MAX_EVENTS
+ * each).  Synchronises the stream. */
+int ctqw_segment_events(ctqw_handle_t h, int64_t r0, int64_t step_lo, int64_t step_hi, ctqw_segment_stats_t *out,
+                        void *stream);
+
+/* Post-processing of npoints collection points at once from their limbs
+ * acc_dev[npoints][3][dim] (all-reduced over ranks beforehand if sharded):
+ * out_dev[npoints][N + 3] = populations (N) + {sum p, sum p^2, participation
+ * ratio}, p = diag / total_count (observables.py:34-101); diag_dev
+ * (optional, [npoints][dim]) receives the diagonal sums.  Four launches for
+ * any number of points; the same bits as ctqw_fixed_to_double +
+ * ctqw_observe_reduce per point. */
+int ctqw_observe_points(ctqw_handle_t h, const int64_t *acc_dev, int64_t npoints, double total_count,
+                        double *out_dev, double *diag_dev, void *stream);
+
 /* Kernel launches issued by this handle since creation (for bench.py). */
 int64_t ctqw_launch_count(ctqw_handle_t h);
 

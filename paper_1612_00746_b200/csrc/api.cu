@@ -62,6 +62,8 @@ struct ctqw_ctx {
   int64_t fixed_cap = 0;
   double* overlap_partial = nullptr;
   int64_t overlap_cap = 0;
+  double* points_scratch = nullptr;  // ctqw_observe_points: per-point partials (+ diag when the caller gives none)
+  int64_t points_cap = 0;
   int64_t last_count = 0;
   std::atomic<long long> launches{0};
   // optional CUDA-event timing of the dominant kernel launches (bench.py)
@@ -381,7 +383,7 @@ int ctqw_destroy(ctqw_handle_t h) {
                       h->summary_dev, h->scratch[0], h->scratch[1], h->n2_dev, h->small,
                       h->overlap_partial, h->tg_values, h->tg_next, h->tg_gen, h->tg_levels, h->tg_sum,
                       h->lat_pos, h->lat_neg, h->t_slot, h->scratch_work, h->fixed_acc,
-                      h->tg_lists, h->tg_oldv};
+                      h->tg_lists, h->tg_oldv, h->points_scratch};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (h->summary_host) cudaFreeHost(h->summary_host);
@@ -672,6 +674,29 @@ int ctqw_check_norm(ctqw_handle_t h, double* psi_dev, int64_t count, const ctqw_
   return CTQW_OK;
 }
 
+namespace {
+
+// Fused collection target of ctqw_evolve_observe (resident64 path only).
+struct ObsTarget {
+  unsigned long long* acc = nullptr;
+  long long post_rate = 1;
+  long long origin = 0;  // the call's first_step: points at origin + k * post_rate and at final_step
+  long long final_step = 0;
+};
+
+// Does this handle's evolve run the N = 64 block kernel (which can fuse the
+// collection into the step)?
+bool uses_resident64(const ctqw_ctx* h, const StepScalars& sc) {
+  return h->stream_kind == 0 && !h->general && resident_supported(h->m, h->n, sc) &&
+         resident64_supported(h->m, h->n, sc) && !std::getenv("CTQW_RESIDENT_STRIP");
+}
+
+int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, int64_t first_step,
+                int64_t n_steps, const ctqw_stepper_t* st, int32_t* result_in_work, cudaStream_t s, bool reset,
+                const ObsTarget& obs);
+
+}  // namespace
+
 int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t count,
                 int64_t first_step, int64_t n_steps, const ctqw_stepper_t* st,
                 int32_t* result_in_work, void* stream) {
@@ -681,14 +706,72 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   rc = check_bound(h, count);
   if (rc) return rc;
   if (n_steps < 0 || first_step < 0) return fail_with(h, CTQW_ERR_CONFIG, "negative step count");
-  if (result_in_work) *result_in_work = 0;
+  DeviceGuard g(h->device);
+  return evolve_impl(h, psi_dev, work_dev, count, first_step, n_steps, st, result_in_work, (cudaStream_t)stream,
+                     true, ObsTarget{});
+}
+
+int ctqw_evolve_observe(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t count, int64_t first_step,
+                        int64_t n_steps, int64_t post_rate, int64_t* acc_dev, const ctqw_stepper_t* st,
+                        int32_t* result_in_work, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  int rc = validate_stepper(h, st);
+  if (rc) return rc;
+  rc = check_bound(h, count);
+  if (rc) return rc;
+  if (n_steps < 1 || first_step < 0 || post_rate < 1)
+    return fail_with(h, CTQW_ERR_CONFIG, "evolve_observe needs n_steps >= 1, first_step >= 0, post_rate >= 1");
+  if (!acc_dev) return fail_with(h, CTQW_ERR_CONFIG, "NULL limb accumulator");
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)stream;
+  const int64_t last = first_step + n_steps;
+  const int64_t npoints = (n_steps + post_rate - 1) / post_rate;
+  CUDA_TRY(h, cudaMemsetAsync(acc_dev, 0, (size_t)npoints * 3 * h->dim * sizeof(int64_t), s));
+  if (result_in_work) *result_in_work = 0;
+  const StepScalars sc = scalars_for(h, st);
+  if (uses_resident64(h, sc)) {
+    ObsTarget o;
+    o.acc = reinterpret_cast<unsigned long long*>(acc_dev);
+    o.post_rate = post_rate;
+    o.origin = first_step;
+    o.final_step = last;
+    return evolve_impl(h, psi_dev, work_dev, count, first_step, n_steps, st, result_in_work, s, true, o);
+  }
+  // every other path: one segment per collection point, then the separate
+  // exact-limb pass over the state (the same bits as the fused form)
+  double* cur = psi_dev;
+  double* other = work_dev;
+  int64_t done = first_step;
+  for (int64_t idx = 0; idx < npoints; ++idx) {
+    const int64_t target = std::min<int64_t>(last, first_step + (idx + 1) * post_rate);
+    int32_t swapped = 0;
+    rc = evolve_impl(h, cur, other, count, done, target - done, st, &swapped, s, idx == 0, ObsTarget{});
+    if (rc) return rc;
+    if (swapped) std::swap(cur, other);
+    done = target;
+    CUDA_TRY(h, launch_observe_diag_fixed((const double2*)cur, count, h->dim,
+                                          reinterpret_cast<unsigned long long*>(acc_dev) + idx * 3 * h->dim, true,
+                                          s));
+    h->launches += 1;
+  }
+  if (result_in_work) *result_in_work = cur == psi_dev ? 0 : 1;
+  return CTQW_OK;
+}
+
+namespace {
+
+int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, int64_t first_step,
+                int64_t n_steps, const ctqw_stepper_t* st, int32_t* result_in_work, cudaStream_t s, bool reset,
+                const ObsTarget& obs) {
+  int rc = CTQW_OK;
+  if (result_in_work) *result_in_work = 0;
   rc = ensure_stats(h, count);
   if (rc) return rc;
   h->last_count = count;
-  CUDA_TRY(h, launch_reset_stats(h->stats, h->scl, count, h->fail, s));
-  h->launches += 1;
+  if (reset) {
+    CUDA_TRY(h, launch_reset_stats(h->stats, h->scl, count, h->fail, s));
+    h->launches += 1;
+  }
   if (count == 0 || n_steps == 0) return CTQW_OK;
   const StepScalars sc = scalars_for(h, st);
   const NormPolicy pol{st->tol_norm, st->tol_fail, st->renormalize};
@@ -703,7 +786,7 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   if (h->stream_kind == 0 && !h->general && resident_supported(h->m, h->n, sc)) {
     // N = 64 with <= 4 applications per step: the 4 x 4-block kernel
     // (resident64.cu); other sizes / orders: the column-strip kernel
-    const bool r64 = resident64_supported(h->m, h->n, sc) && !std::getenv("CTQW_RESIDENT_STRIP");
+    const bool r64 = uses_resident64(h, sc);
     h->stream_kernel = r64 ? "resident64_kernel" : "resident_kernel";
     std::snprintf(h->variant, sizeof(h->variant), "%s<%s,order=%d,site=%d,exact=%d,N=%d>", h->stream_kernel,
                   sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", sc.order, coef.site != nullptr ? 1 : 0,
@@ -714,7 +797,7 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
       timing_event(h, s);
       if (r64)
         CUDA_TRY(h, launch_resident64(psi, count, coef, h->k, sc, exact, pol, first_step + j, chunk, h->stats,
-                                      h->events, h->fail, s));
+                                      h->events, h->fail, s, obs.acc, obs.post_rate, obs.origin, obs.final_step));
       else
         CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step + j, chunk,
                                     h->stats, h->events, h->fail, s));
@@ -830,6 +913,8 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
   h->launches += 2;
   return CTQW_OK;
 }
+
+}  // namespace
 
 int ctqw_segment_stats(ctqw_handle_t h, int64_t r0, ctqw_segment_stats_t* out, void* stream) {
   if (!h || !out) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");
@@ -971,6 +1056,64 @@ int ctqw_packed_gram(const double* psi_dev, int64_t count, int64_t dim, double s
   DeviceGuard g(device);
   CUDA_TRY(nullptr, launch_packed_gram((const double2*)psi_dev, count, dim, scale, (double2*)packed_dev,
                                        (cudaStream_t)stream));
+  return CTQW_OK;
+}
+
+int ctqw_segment_events(ctqw_handle_t h, int64_t r0, int64_t step_lo, int64_t step_hi, ctqw_segment_stats_t* out,
+                        void* stream) {
+  if (!h || !out) return fail_with(h, CTQW_ERR_CONFIG, "NULL argument");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::memset(out, 0, sizeof(*out));
+  const int64_t count = h->last_count;
+  CUDA_TRY(h, cudaStreamSynchronize(s));
+  if (count == 0) return CTQW_OK;
+  std::vector<RealStat> stats(count);
+  std::vector<EventRec> evs((size_t)count * kMaxEvents);
+  CUDA_TRY(h, cudaMemcpy(stats.data(), h->stats, count * sizeof(RealStat), cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaMemcpy(evs.data(), h->events, (size_t)count * kMaxEvents * sizeof(EventRec),
+                         cudaMemcpyDeviceToHost));
+  struct Item {
+    long long step;
+    int64_t r;
+    double dev;
+    int corrected;
+  };
+  std::vector<Item> items;
+  for (int64_t r = 0; r < count; ++r)
+    for (int e = 0; e < stats[r].n_ev; ++e) {
+      const EventRec& rec = evs[(size_t)r * kMaxEvents + e];
+      if (rec.step_lo > step_lo && rec.step_lo <= step_hi) items.push_back(Item{rec.step_lo, r, rec.dev, rec.corrected});
+    }
+  const size_t keep = std::min<size_t>(items.size(), CTQW_MAX_EVENTS);
+  std::partial_sort(items.begin(), items.begin() + keep, items.end(), [](const Item& a, const Item& b) {
+    return a.step != b.step ? a.step < b.step : a.r < b.r;
+  });
+  for (size_t i = 0; i < keep; ++i) {
+    out->events[i].deviation = items[i].dev;
+    out->events[i].realization = r0 + items[i].r;
+    out->events[i].step = items[i].step;
+    out->events[i].corrected = items[i].corrected;
+  }
+  out->n_events = (int32_t)keep;
+  out->event_count = (int64_t)items.size();
+  return CTQW_OK;
+}
+
+int ctqw_observe_points(ctqw_handle_t h, const int64_t* acc_dev, int64_t npoints, double total_count,
+                        double* out_dev, double* diag_dev, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (npoints < 0 || npoints > 65535) return fail_with(h, CTQW_ERR_CONFIG, "npoints must be in [0, 65535]");
+  if (npoints == 0) return CTQW_OK;
+  if (!acc_dev || !out_dev) return fail_with(h, CTQW_ERR_CONFIG, "NULL buffer");
+  DeviceGuard g(h->device);
+  int rc = ensure(h, &h->points_scratch, &h->points_cap, npoints * 148 * 2 + (diag_dev ? 0 : npoints * h->dim),
+                  "collection-point scratch");
+  if (rc) return rc;
+  double* diag = diag_dev ? diag_dev : h->points_scratch + npoints * 148 * 2;
+  CUDA_TRY(h, launch_observe_points(h->m, h->n, h->dim, reinterpret_cast<const unsigned long long*>(acc_dev), npoints,
+                                    total_count, diag, out_dev, h->points_scratch, (cudaStream_t)stream));
+  h->launches += 4;
   return CTQW_OK;
 }
 

@@ -150,4 +150,33 @@ __device__ __forceinline__ double norm_decide(double n2, long long step, const N
   return 1.0;
 }
 
+// Exact (order-independent) ensemble sums of |psi_r(alpha)|^2.
+//
+// Each term x = |psi|^2 (x <= 2^22) is split, exactly and deterministically,
+// into three pieces on the fixed grids 2^-30, 2^-70 and 2^-110
+// (x = a2 + a1 + a0 + (rounding below 2^-111)), and each piece is added as an
+// int64 multiple of its grid: limb k of [3][dim].  Integer addition is
+// associative, so the sum is the same bits for any realization order, any
+// split of the realizations over blocks, atomics or GPUs (the all-reduce of
+// the limbs is an int64 SUM).  This is what makes the observables identical
+// across 1/2/4/8 GPUs, as the reference's are across worker counts
+// (pkg/README.md:174-180).  Limbs hold up to 2^23 realizations without
+// overflow.  Terms below 2^-111 (far beneath the 1e-10 relative bar on any
+// entry above 1e-30) are dropped.
+__device__ __forceinline__ void fixed_split(double x, long long& l2, long long& l1, long long& l0) {
+  const double c2 = 0x1.8p22, c1 = 0x1.8p-18, c0 = 0x1.8p-58;
+  const double a2 = __dsub_rn(__dadd_rn(x, c2), c2);  // nearest multiple of 2^-30
+  const double r1 = __dsub_rn(x, a2);                 // exact
+  const double a1 = __dsub_rn(__dadd_rn(r1, c1), c1); // nearest multiple of 2^-70
+  const double r0 = __dsub_rn(r1, a1);                // exact
+  const double a0 = __dsub_rn(__dadd_rn(r0, c0), c0); // nearest multiple of 2^-110
+  l2 = __double2ll_rn(__dmul_rn(a2, 0x1p30));
+  l1 = __double2ll_rn(__dmul_rn(a1, 0x1p70));
+  l0 = __double2ll_rn(__dmul_rn(a0, 0x1p110));
+}
+
+// |z|^2 = re*re + im*im, each product rounded (no FMA contraction), as NumPy
+// forms it: the term -- and so its limbs -- is a pure function of z.
+__device__ __forceinline__ double norm2_rn(double2 z) { return __dadd_rn(__dmul_rn(z.x, z.x), __dmul_rn(z.y, z.y)); }
+
 }  // namespace ctqw

@@ -104,7 +104,13 @@ bool resident64_supported(int m, int n, const StepScalars& sc);
 cudaError_t launch_resident64(double2* psi, int64_t count, const Coef& coef, const StencilConst& k,
                               const StepScalars& sc, bool exact, const NormPolicy& pol, long long first_step,
                               long long n_steps, RealStat* stats, EventRec* events, long long* fail,
-                              cudaStream_t s);
+                              cudaStream_t s, unsigned long long* obs = nullptr, long long post_rate = 1,
+                              long long origin = 0, long long final_step = 0);
+// Batched post-processing of P collection points from their exact limbs
+// acc[P][3][dim]: diag[P][dim] (scratch or the caller's), out[P][n + 3] =
+// populations (n) + {sum p, sum p^2, participation ratio}.
+cudaError_t launch_observe_points(int m, int n, int64_t dim, const unsigned long long* acc, int64_t npoints,
+                                  double total, double* diag, double* out, double* scratch, cudaStream_t s);
 int tile_parts(int n, const StepScalars& sc);
 cudaError_t launch_tile_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
                              const Coef& coef, const StencilConst& k, const StepScalars& sc,

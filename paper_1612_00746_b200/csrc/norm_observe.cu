@@ -130,34 +130,8 @@ __global__ void norm_sum_kernel(const double* __restrict__ partial, int nparts, 
   n2[r] = s;
 }
 
-// Exact (order-independent) ensemble sums of |psi_r(alpha)|^2.
-//
-// Each term x = |psi|^2 (x <= 2^22) is split, exactly and deterministically,
-// into three pieces on the fixed grids 2^-30, 2^-70 and 2^-110
-// (x = a2 + a1 + a0 + (rounding below 2^-111)), and each piece is added as an
-// int64 multiple of its grid: limb k of [3][dim].  Integer addition is
-// associative, so the sum is the same bits for any realization order, any
-// split of the realizations over blocks, atomics or GPUs (the all-reduce of
-// the limbs is an int64 SUM).  This is what makes the observables identical
-// across 1/2/4/8 GPUs, as the reference's are across worker counts
-// (pkg/README.md:174-180).  Limbs hold up to 2^23 realizations without
-// overflow.  Terms below 2^-111 (far beneath the 1e-10 relative bar on any
-// entry above 1e-30) are dropped.
-__device__ __forceinline__ void fixed_split(double x, long long& l2, long long& l1, long long& l0) {
-  const double c2 = 0x1.8p22, c1 = 0x1.8p-18, c0 = 0x1.8p-58;
-  const double a2 = __dsub_rn(__dadd_rn(x, c2), c2);  // nearest multiple of 2^-30
-  const double r1 = __dsub_rn(x, a2);                 // exact
-  const double a1 = __dsub_rn(__dadd_rn(r1, c1), c1); // nearest multiple of 2^-70
-  const double r0 = __dsub_rn(r1, a1);                // exact
-  const double a0 = __dsub_rn(__dadd_rn(r0, c0), c0); // nearest multiple of 2^-110
-  l2 = __double2ll_rn(__dmul_rn(a2, 0x1p30));
-  l1 = __double2ll_rn(__dmul_rn(a1, 0x1p70));
-  l0 = __double2ll_rn(__dmul_rn(a0, 0x1p110));
-}
-
-// |z|^2 = re*re + im*im, each product rounded (no FMA contraction), as NumPy
-// forms it: the term -- and so its limbs -- is a pure function of z.
-__device__ __forceinline__ double norm2_rn(double2 z) { return __dadd_rn(__dmul_rn(z.x, z.x), __dmul_rn(z.y, z.y)); }
+// fixed_split / norm2_rn: ctqw_device.cuh (shared with the fused
+// collection of resident64.cu)
 
 // acc[k][alpha] += sum_{r in this block's realization range} limb_k(|psi_r(alpha)|^2)
 __global__ void observe_diag_fixed_kernel(const double2* __restrict__ psi, int64_t count, int64_t dim,
@@ -458,6 +432,94 @@ cudaError_t launch_observe_reduce(int m, int n, int64_t dim, const double* diag_
   const int nparts = 148;
   joint_sums_kernel<<<nparts, 256, 0, s>>>(diag_sum, dim, total, scratch, joint);
   joint_final_kernel<<<1, 32, 0, s>>>(scratch, nparts, scalars);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Batched post-processing of P collection points (ctqw_observe_points): the
+// per-point kernels above with the point on blockIdx.y, four launches for
+// any number of points.
+
+__global__ void fixed_to_double_points_kernel(const unsigned long long* __restrict__ acc, int64_t dim,
+                                              double* __restrict__ diag) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= dim) return;
+  const unsigned long long* ap = acc + (int64_t)blockIdx.y * 3 * dim;
+  long long l2 = (long long)ap[a], l1 = (long long)ap[dim + a], l0 = (long long)ap[2 * dim + a];
+  const long long c0 = l0 >> 40;
+  l0 -= c0 << 40;
+  l1 += c0;
+  const long long c1 = l1 >> 40;
+  l1 -= c1 << 40;
+  l2 += c1;
+  const double lo = __dadd_rn(__dmul_rn((double)l1, 0x1p-70), __dmul_rn((double)l0, 0x1p-110));
+  diag[(int64_t)blockIdx.y * dim + a] = __dadd_rn(__dmul_rn((double)l2, 0x1p-30), lo);
+}
+
+__global__ void populations_points_kernel(int m, int n, int64_t dim, const double* __restrict__ diag, double total,
+                                          double* out, int64_t out_stride) {
+  __shared__ double red[32];
+  const int x = blockIdx.x;
+  const double* dp = diag + (int64_t)blockIdx.y * dim;
+  const int64_t plane = m == 1 ? 1 : (m == 2 ? (int64_t)n : (int64_t)n * n);
+  double acc = 0.0;
+  for (int p = 0; p < m; ++p) {
+    int64_t stride_p = 1;
+    for (int q = p + 1; q < m; ++q) stride_p *= n;
+    for (int64_t j = threadIdx.x; j < plane; j += blockDim.x) {
+      const int64_t low = j % stride_p, high = j / stride_p;
+      acc += dp[(high * n + x) * stride_p + low] / total;
+    }
+  }
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) out[(int64_t)blockIdx.y * out_stride + x] = b;
+}
+
+__global__ void joint_sums_points_kernel(const double* __restrict__ diag, int64_t dim, double total,
+                                         double* partial) {
+  __shared__ double red[32];
+  const double* dp = diag + (int64_t)blockIdx.y * dim;
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < dim; a += (int64_t)gridDim.x * blockDim.x) {
+    const double p = dp[a] / total;
+    s1 += p;
+    s2 += p * p;
+  }
+  const double b1 = block_sum(s1, red);
+  const double b2 = block_sum(s2, red);
+  if (threadIdx.x == 0) {
+    double* pp = partial + (int64_t)blockIdx.y * 2 * gridDim.x;
+    pp[2 * blockIdx.x] = b1;
+    pp[2 * blockIdx.x + 1] = b2;
+  }
+}
+
+__global__ void joint_final_points_kernel(const double* __restrict__ partial, int nparts, double* out,
+                                          int64_t out_stride, int n) {
+  if (threadIdx.x != 0) return;
+  const double* pp = partial + (int64_t)blockIdx.x * 2 * nparts;
+  double s1 = 0.0, s2 = 0.0;
+  for (int i = 0; i < nparts; ++i) {
+    s1 += pp[2 * i];
+    s2 += pp[2 * i + 1];
+  }
+  double* o = out + (int64_t)blockIdx.x * out_stride + n;
+  o[0] = s1;
+  o[1] = s2;
+  o[2] = s2 > 0.0 ? (s1 * s1) / s2 : (s2 == s2 ? __longlong_as_double(0x7ff8000000000000LL) : s2);
+}
+
+cudaError_t launch_observe_points(int m, int n, int64_t dim, const unsigned long long* acc, int64_t npoints,
+                                  double total, double* diag, double* out, double* scratch, cudaStream_t s) {
+  if (npoints <= 0) return cudaSuccess;
+  if (npoints > 65535) return cudaErrorInvalidValue;
+  const unsigned P = (unsigned)npoints;
+  const int nparts = 148;
+  const int64_t stride = n + 3;
+  fixed_to_double_points_kernel<<<dim3((unsigned)((dim + 255) / 256), P), 256, 0, s>>>(acc, dim, diag);
+  populations_points_kernel<<<dim3((unsigned)n, P), 256, 0, s>>>(m, n, dim, diag, total, out, stride);
+  joint_sums_points_kernel<<<dim3(nparts, P), 256, 0, s>>>(diag, dim, total, scratch);
+  joint_final_points_kernel<<<P, 32, 0, s>>>(scratch, nparts, out, stride, n);
   return cudaGetLastError();
 }
 

@@ -45,6 +45,13 @@ struct Res64Args {
   RealStat* stats;
   EventRec* events;
   long long* fail;
+  // fused collection (ctqw_evolve_observe): at every global step g with
+  // (g - origin) % post_rate == 0 or g == final_step, the exact limbs of
+  // |psi_r(g)|^2 are added into obs[idx][3][N^2], idx = ceil((g - origin) / post_rate) - 1
+  unsigned long long* obs;
+  long long post_rate;
+  long long origin;
+  long long final_step;
 };
 
 // 16-byte chunk x of row y at x ^ ((x >> 3) & 3): the block-row loads
@@ -221,6 +228,28 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
         if (RK4) psis[zo(y0 + i, x0 + q)] = cur[i][q];
       }
     if (scl != 1.0 || RK4) __syncthreads();
+    if (a.obs) {
+      // diag(rho) fused into the step (ensemble.py:761-769, density.py:91-95):
+      // this realization's |psi|^2 as exact int64 limbs, added with L2
+      // reductions -- integer addition, so the sum's bits do not depend on
+      // the order the realizations arrive in
+      const long long gs = a.first_step + step + 1, rel = gs - a.origin;
+      if (rel % a.post_rate == 0 || gs == a.final_step) {
+        const long long idx = (rel + a.post_rate - 1) / a.post_rate - 1;
+        unsigned long long* o = a.obs + idx * 3 * (int64_t)kPlane64;
+#pragma unroll
+        for (int i = 0; i < kB64; ++i)
+#pragma unroll
+          for (int q = 0; q < kB64; ++q) {
+            long long l2, l1, l0;
+            fixed_split(norm2_rn(cur[i][q]), l2, l1, l0);
+            const int al = (y0 + i) * kN64 + x0 + q;
+            atomicAdd(o + al, (unsigned long long)l2);
+            atomicAdd(o + kPlane64 + al, (unsigned long long)l1);
+            atomicAdd(o + 2 * kPlane64 + al, (unsigned long long)l0);
+          }
+      }
+    }
   }
 #pragma unroll
   for (int i = 0; i < kB64; ++i)
@@ -278,8 +307,13 @@ bool resident64_supported(int m, int n, const StepScalars& sc) {
 cudaError_t launch_resident64(double2* psi, int64_t count, const Coef& coef, const StencilConst& k,
                               const StepScalars& sc, bool exact, const NormPolicy& pol, long long first_step,
                               long long n_steps, RealStat* stats, EventRec* events, long long* fail,
-                              cudaStream_t s) {
+                              cudaStream_t s, unsigned long long* obs, long long post_rate, long long origin,
+                              long long final_step) {
   Res64Args a;
+  a.obs = obs;
+  a.post_rate = post_rate > 0 ? post_rate : 1;
+  a.origin = origin;
+  a.final_step = final_step;
   a.psi = psi;
   a.r_base = 0;
   a.coef = coef;

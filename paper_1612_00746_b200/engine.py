@@ -434,6 +434,24 @@ class EnsembleState:
         if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
 
+    def evolve_observe(self, first_step: int, n_steps: int, post_rate: int, acc):
+        """Enqueue ``n_steps`` steps and the collection points among them
+        (every ``post_rate``-th step from ``first_step``, and the last one): acc[P][3][D]
+        int64 receives each point's exact limbs of sum_r |psi_r|^2
+        (ctqw_evolve_observe; fused into the step kernel on the resident
+        N = 64 path)."""
+        if self.count == 0:
+            acc.zero_()
+            return
+        swapped = self.handle.evolve_observe(self.psi, self.work, self.count, first_step, n_steps, post_rate, acc,
+                                             self.stepper)
+        if swapped and self.work is not self.psi:
+            self.psi, self.work = self.work, self.psi
+
+    def segment_events(self, step_lo: int, step_hi: int) -> list:
+        st = self.handle.segment_events(self.lo, step_lo, step_hi)
+        return [(e.deviation, bool(e.corrected), int(e.realization), int(e.step)) for e in st.events[: st.n_events]]
+
     def stats(self) -> dict:
         st = self.handle.segment_stats(self.lo)
         events = [(e.deviation, bool(e.corrected), int(e.realization), int(e.step))
@@ -585,6 +603,95 @@ def collect_observables(config, ens: EnsembleState, group=None, want_joint=None)
     return obs.populations, obs.participation_ratio, obs.purity, obs.joint(), obs.diag_dev
 
 
+# steps per evolve_observe call in run(): each realization logs at most one
+# event per step and keeps CTQW_MAX_EVENTS of them, so with calls of at most
+# this many steps every segment's event list can be rebuilt exactly
+FUSED_CALL_STEPS = MAX_EVENTS_PER_SEGMENT
+FUSED_ACC_BYTES = 512 * 2**20
+
+
+def fused_collection_ok(config: RunConfig, sinks, world: int) -> bool:
+    """run() takes the batched path (ctqw_evolve_observe + ctqw_observe_points:
+    one call per group of collection points instead of a segment call, a
+    limb pass and four reductions per point) unless a point needs the states
+    themselves (purity, the dense rho) or the run is sharded."""
+    return (world == 1 and OBS_PURITY not in config.observables and not getattr(sinks, "dense_density", False)
+            and config.steps > 0)
+
+
+def _fused_groups(config: RunConfig):
+    """Consecutive schedule points grouped into evolve_observe calls."""
+    dim = config.space.dim
+    max_points = max(1, FUSED_ACC_BYTES // (24 * dim))
+    groups, cur, start = [], [], 0
+    for t in config.schedule:
+        if cur and (t - start > FUSED_CALL_STEPS or len(cur) >= max_points):
+            groups.append((start, cur))
+            start, cur = cur[-1], []
+        cur.append(t)
+    if cur:
+        groups.append((start, cur))
+    return groups
+
+
+def _run_fused(config, ens, sinks, emit, profile, clock):
+    """The schedule loop of run() on the batched path; same rows, events,
+    counters and failure semantics as the per-segment loop."""
+    import torch
+
+    n = config.space.lattice.n_sites
+    dim = config.space.dim
+    want_joint = OBS_JOINT in config.observables
+    totals = {"corrections": 0, "events": 0, "max_dev": 0.0, "snapshots": 0}
+    for start, targets in _fused_groups(config):
+        npts = len(targets)
+        t0 = clock()
+        acc = torch.empty((npts, 3, dim), dtype=torch.int64, device=ens.dev)
+        ens.evolve_observe(start, targets[-1] - start, config.post_rate, acc)
+        out = torch.empty((npts, n + 3), dtype=torch.float64, device=ens.dev)
+        diag = torch.empty((npts, dim), dtype=torch.float64, device=ens.dev)
+        ens.handle.observe_points(acc, npts, float(config.realizations), out, diag)
+        local = ens.stats()  # synchronises
+        host = out.cpu().numpy()
+        profile.add(STAGE_EVOLUTION, clock() - t0, calls=config.realizations * (targets[-1] - start))
+        profile.add(STAGE_HAMILTONIAN, 0.0, calls=config.realizations * (targets[-1] - start))
+        fail = local["failure"]
+        previous = start
+        for k, target in enumerate(targets):
+            if fail is not None and fail[2] <= target:
+                dev, real, step = fail
+                emit(sinks.message, f"aborted: norm deviation {dev:.3e} at realization {real}, step {step}; "
+                                    f"reduce the time step")
+                ens.release()
+                raise NormFailureError(dev, realization=real, step=step)
+            events = ens.segment_events(previous, target) if local["event_count"] else []
+            if events:
+                emit(sinks.norm_events, [NormEvent(deviation=d, corrected=c, realization=r, step=s)
+                                         for d, c, r, s in events])
+            with profile.stage(STAGE_DENSITY):
+                pops = host[k, :n].copy()
+                s2 = float(host[k, n + 1])
+                if s2 <= 0.0:
+                    raise NumericError("joint distribution has no weight")
+                pr = float(host[k, n + 2])
+                # p = diag / R divided as the reduction kernel does (IEEE division,
+                # not torch's reciprocal multiply)
+                joint = diag[k].cpu().numpy() / float(config.realizations) if want_joint else None
+                time_tag = target * config.stepper.dt
+                rows = _observable_rows(config, pops, pr, None, joint)
+                rho = DiagonalDensity(diag=None, dim=dim, sample_count=config.realizations,
+                                      time_tag=float(time_tag), purity=None, populations=pops,
+                                      participation_ratio=pr, device_diag=diag[k])
+            totals["snapshots"] += 1
+            emit(sinks.observable_rows, rho.time_tag, rows)
+            emit(sinks.density_snapshot, rho, target)
+            previous = target
+        totals["corrections"] += local["corrections"]
+        totals["events"] += local["event_count"]
+        totals["max_dev"] = max(totals["max_dev"], local["max_deviation"])
+    return totals
+
+
 def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunReport:
     """Execute a full ensemble run on the GPU(s) (ensemble.py:635-804)."""
     import torch
@@ -640,8 +747,14 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
     corrections = 0
     event_total = 0
     previous = 0
+    fused = fused_collection_ok(config, sinks, world)
+    if fused:
+        with torch.cuda.device(device):
+            tot = _run_fused(config, ens, sinks, emit, profile, clock)
+        snapshots, corrections = tot["snapshots"], tot["corrections"]
+        event_total, max_deviation = tot["events"], tot["max_dev"]
     with torch.cuda.device(device):
-        for target in config.schedule:
+        for target in (() if fused else config.schedule):
             span = target - previous
             if span > 0:
                 t0 = clock()

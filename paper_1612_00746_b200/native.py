@@ -108,6 +108,10 @@ SIGNATURES = {
     "ctqw_observe_reduce": (ctypes.c_int, [_P, _P, _D, _P, _P, _P, _P]),
     "ctqw_overlap_sumsq": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
     "ctqw_packed_gram": (ctypes.c_int, [_P, _I64, _I64, _D, _P, _I32, _P]),
+    "ctqw_evolve_observe": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, ctypes.POINTER(Stepper),
+                                           ctypes.POINTER(_I32), _P]),
+    "ctqw_segment_events": (ctypes.c_int, [_P, _I64, _I64, _I64, ctypes.POINTER(SegmentStats), _P]),
+    "ctqw_observe_points": (ctypes.c_int, [_P, _P, _I64, _D, _P, _P, _P]),
     "ctqw_launch_count": (ctypes.c_int64, [_P]),
     "ctqw_kernel_timing": (ctypes.c_int, [_P, _I32]),
     "ctqw_kernel_time": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
@@ -315,6 +319,24 @@ class Handle:
                                          int(first_step), int(n_steps), ctypes.byref(stepper),
                                          ctypes.byref(flag), self.stream))
         return bool(flag.value)
+
+    def evolve_observe(self, psi, work, count: int, first_step: int, n_steps: int, post_rate: int, acc,
+                       stepper: Stepper) -> bool:
+        flag = _I32(0)
+        self._check(self.lib.ctqw_evolve_observe(self._h, _ptr(psi), _ptr(work), int(count), int(first_step),
+                                                 int(n_steps), int(post_rate), _ptr(acc), ctypes.byref(stepper),
+                                                 ctypes.byref(flag), self.stream))
+        return bool(flag.value)
+
+    def segment_events(self, r0: int, step_lo: int, step_hi: int) -> SegmentStats:
+        st = SegmentStats()
+        self._check(self.lib.ctqw_segment_events(self._h, int(r0), int(step_lo), int(step_hi), ctypes.byref(st),
+                                                 self.stream))
+        return st
+
+    def observe_points(self, acc, npoints: int, total: float, out, diag=None):
+        self._check(self.lib.ctqw_observe_points(self._h, _ptr(acc), int(npoints), float(total), _ptr(out),
+                                                 _ptr(diag), self.stream))
 
     def segment_stats(self, r0: int = 0) -> SegmentStats:
         st = SegmentStats()
