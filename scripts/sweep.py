@@ -26,17 +26,28 @@ ONLY = ""
 
 
 def timed(ens, cfg, steps, post_rate, engine, torch):
+    """Device seconds of ``steps`` steps with a collection point every
+    ``post_rate`` steps, the way run() schedules them: the batched path
+    (ctqw_evolve_observe + ctqw_observe_points, bench.enqueue_schedule), or
+    per segment when purity (which needs the states) is requested."""
+    import dataclasses
+
+    import bench
+
+    c = dataclasses.replace(cfg, steps=steps, post_rate=post_rate)
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     start.record()
-    done = 0
-    while done < steps:
-        span = min(post_rate, steps - done)
-        ens.evolve(done, span)
-        done += span
-        if post_rate < steps or done == steps:
-            engine.collect_observables(cfg, ens)
+    if engine.OBS_PURITY in c.observables:
+        done = 0
+        while done < steps:
+            span = min(post_rate, steps - done)
+            ens.evolve(done, span)
+            done += span
+            engine.collect_observables(c, ens)
+    else:
+        bench.enqueue_schedule(engine, c, ens, 0, steps, torch)
     stop.record()
     torch.cuda.synchronize()
     st = ens.stats()
@@ -68,6 +79,7 @@ def run_case(name, m, n, R, steps, backend="taylor", dt=0.02, target="tunneling"
         ens.evolve(0, 1)
         for pr in post_rates:
             prate = steps if pr is None else pr
+            timed(ens, cfg, steps, prate, engine, torch)  # untimed: allocator, scratch, first launches
             secs = timed(ens, cfg, steps, prate, engine, torch)
             thr = R * steps / secs
             line = {"case": name, "m": m, "n": n, "realizations": R, "steps": steps, "backend": backend,
@@ -92,6 +104,7 @@ def main():
     # configs[0]: N=64, 100 realizations (resident kernel), Taylor, post every 10 steps
     run_case("configs[0] N=64 R=100", 2, 64, 100, 300 if q else 1500, post_rates=(10, None),
              observables=("populations", "position_mean_variance", "purity", "participation_ratio"))
+    run_case("configs[0] N=64 R=100 diag observables", 2, 64, 100, 300 if q else 1500, post_rates=(10, None))
     run_case("N=64 R=1000", 2, 64, 1000, 300 if q else 1500)
     # configs[1]: N=256, 1000 realizations, Taylor vs RK4
     for backend in ("taylor", "rk4"):
