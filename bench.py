@@ -548,6 +548,11 @@ def secondary_line(p, engine, a, local, world, torch, barrier, all_max, group):
 
 
 def ours(a):
+    # the JSON line is the only thing on stdout: libraries that print there
+    # (NCCL's version banner at communicator init, ...) go to stderr
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     import torch
     import torch.distributed as dist
 
@@ -758,7 +763,7 @@ def ours(a):
             "clocks": clocks.summary(),
             "norm_events": stats["event_count"],
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=json_out, flush=True)
     if distributed:
         dist.destroy_process_group()
 
@@ -774,6 +779,7 @@ def launch_ranks(a):
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
     return subprocess.call(cmd + sys.argv[1:], env=env)
@@ -788,6 +794,7 @@ def main():
     else:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
         ours(a)
 
 
