@@ -25,8 +25,41 @@ def run(m, n, R, steps, backend="taylor", rate=0.0, target="both", lattice=None,
     print(m, n, R, backend, rate, stream, "rows", len(sinks.rows), "ok", flush=True)
 
 
+def gram():
+    import torch
+
+    from paper_1612_00746_b200 import density
+
+    rng = np.random.default_rng(3)
+    stack = torch.as_tensor(rng.normal(size=(5, 70)) + 1j * rng.normal(size=(5, 70)), device="cuda:0")
+    density.packed_density_device(stack, 5)
+    torch.cuda.synchronize()
+    print("packed_gram ok", flush=True)
+
+
+def run_posts(m, n, R, steps, post, backend="taylor", rate=0.0, dt=0.05):
+    """run() on the batched schedule: evolve_observe (fused on resident64),
+    observe_points, segment events."""
+    cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([n]), m), model=p.CouplingModel(onsite_energy=0.1),
+                      noise=p.NoiseSpec(target="both", rate=rate), stepper=p.StepperConfig(backend=backend, dt=dt),
+                      realizations=R, steps=steps, post_rate=post, precision="double",
+                      observables=("populations", "participation_ratio", "joint_distribution"))
+    sinks = p.MemorySinks()
+    p.run(cfg, sinks)
+    print(m, n, R, backend, "post", post, "rows", len(sinks.rows), "events", len(sinks.events), "ok", flush=True)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["band4", "resident", "generic", "telegraph", "lattice", "plane3"]
+    which = sys.argv[1:] or ["band4", "resident", "generic", "telegraph", "lattice", "plane3", "resident64",
+                             "gram", "points"]
+    if "resident64" in which:
+        run(2, 64, 2, 3)
+        run(2, 64, 2, 3, "rk4")
+        run_posts(2, 64, 2, 9, 3, dt=0.12)  # fused collection, with renormalisations
+    if "gram" in which:
+        gram()
+    if "points" in which:
+        run_posts(2, 96, 2, 6, 2)
     if "band4" in which:
         run(2, 96, 3, 3)
         run(2, 256, 2, 2, "rk4")
