@@ -133,6 +133,7 @@ struct T4 {
   int NP;
   double hc[kCols];   // register copy of the column couplings (kColcRegs)
   double hm0;
+  double sx[kCols];   // register copy of site[4p+q] (Taylor with on-site noise)
 };
 
 // Column tunnelling couplings: in registers (10 registers, no loads) for the
@@ -160,7 +161,7 @@ __device__ __forceinline__ ColC load_colc(const T4& T) {
     c.hm0 = T.colc[kCols * T.NP + T.p];
   }
 #pragma unroll
-  for (int q = 0; q < kCols; ++q) c.sx[q] = SITE ? T.colc[(kCols + 1 + q) * T.NP + T.p] : 0.0;
+  for (int q = 0; q < kCols; ++q) c.sx[q] = SITE ? (CREG ? T.sx[q] : T.colc[(kCols + 1 + q) * T.NP + T.p]) : 0.0;
   return c;
 }
 
@@ -623,7 +624,10 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
       }
       cc[kCols * NP + p] = hop[g.wrap(kCols * p - 1)];
 #pragma unroll
-      for (int q = 0; q < kCols; ++q) T.hc[q] = hop[kCols * p + q];
+      for (int q = 0; q < kCols; ++q) {
+        T.hc[q] = hop[kCols * p + q];
+        T.sx[q] = SITE ? sg[kCols * p + q] : 0.0;
+      }
       T.hm0 = hop[g.wrap(kCols * p - 1)];
     }
     P.s = a.scl ? a.scl[r] : 1.0;
