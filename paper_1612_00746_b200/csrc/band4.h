@@ -46,7 +46,7 @@ struct Band4Plan {
 // Does the RK4 stash fit next to the rest (compile-time sizes only)?
 constexpr bool stash_fits(int nn, bool site) {
   return nn > 0 && (size_t)kRing4 * nn * 16 + (size_t)3 * 4 * (nn / 4) * 16 + (size_t)nn * 16 +
-                           (size_t)((site ? nn : 0) + 64 + (site ? 9 : 5) * (nn / 4)) * 8 + kRing4 * 8 + 16 +
+                           (size_t)((site ? nn : 0) + 64 + (site ? 9 : 5) * (nn / 4)) * 8 + (kRing4 + 2) * 8 + 16 +
                            (size_t)4 * (nn / 4) * 16 <=
                        227 * 1024;
 }

@@ -92,6 +92,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive4(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Split-phase row barrier for the one-CTA-per-SM size (n = 1024, 8 warps):
+// every thread
+// arrives at the end of its iteration and waits for everybody's arrival only
+// after computing the next iteration's stage 1 (which reads nothing another
+// warp writes), so stage 1 fills the time a warp would idle at a
+// __syncthreads.  Two mbarriers alternate by iteration parity; a warp can
+// be at most one iteration ahead of the slowest, so a parity wait is exact.
+// (At n = 512, two CTAs share an SM and hide each other's __syncthreads;
+// the mbarrier form measured 7 % slower there.)
+template <int NN>
+constexpr bool band4_split() {
+  return NN >= 1024;
+}
+
 // One psi row (n complex = n/8 lines of 128 B) global -> shared through TMA,
 // 128B-swizzled: 16-byte chunk c lands at chunk c ^ ((c >> 3) & 7), which is
 // swz(c) because the destination slot is 1024-byte aligned.
@@ -173,6 +191,7 @@ struct Piece4 {
   double s;
   bool scale;
   int pend;           // norm block awaiting its flush (-1 none)
+  int g0;             // CTA iteration count before this piece (split barrier phases)
   int64_t grow0;      // TMA row coordinate of psi row 0 of this realization (r * n)
   uint32_t* ph;       // per-slot mbarrier phase bits (TMA path)
 };
@@ -201,8 +220,10 @@ struct Lay4 {
   }
   // RK4: acc(j) = psi(j) + k1/6 parked from stage 1 to the end of the iteration
   // ([q][NP], private per thread), instead of 16 registers across stages 2-4
+  // split-phase row barrier (band4_split): mbarriers [iteration & 1]
+  __device__ __forceinline__ static uint64_t* rowbar(const Geo4<NN>& g) { return bars(g) + kRing4; }
   __device__ __forceinline__ static double2* stash(const Geo4<NN>& g) {
-    const uintptr_t b = reinterpret_cast<uintptr_t>(bars(g) + kRing4);
+    const uintptr_t b = reinterpret_cast<uintptr_t>(bars(g) + kRing4 + 2);
     return reinterpret_cast<double2*>((b + 15) & ~uintptr_t(15));
   }
 };
@@ -458,14 +479,17 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
   const int j = P.j0 + i;
   // rho = i + 2 (psi(j+1)) must have landed; the barrier also publishes the
   // neighbour columns of the last iteration and retires its ring reads.
+  constexpr bool SPLIT = band4_split<NN>();
   if constexpr (NN > 0) {
     band4_wait_row<NN>(P, i + 2, bars);
   } else {
     cpa_wait<kPref4 - 2>();
   }
-  __syncthreads();
-  band4_flush<NN, NAPP, SITE>(g, T, P);
-  if (i + kPref4 + 1 <= P.last_rho) band4_load_row(a, g, T, P, i + kPref4 + 1, bars);
+  if constexpr (!SPLIT) {
+    __syncthreads();
+    band4_flush<NN, NAPP, SITE>(g, T, P);
+    if (i + kPref4 + 1 <= P.last_rho) band4_load_row(a, g, T, P, i + kPref4 + 1, bars);
+  }
   if constexpr (NN == 0) cpa_commit();
   const int buf = i & 1;
   constexpr double c16 = 1.0 / 6.0;
@@ -531,6 +555,15 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
       nt = t;
     }
     R.w[1][PH] = nt;
+    if constexpr (SPLIT) {
+      // everybody finished iteration i-1: its exchange rows are published,
+      // the exchange buffer this stage overwrites and the ring slot the next
+      // TMA refills are no longer read, its norm-block partials are in place
+      const int G = P.g0 + i;
+      if (i > 0) mbar_wait(smem_u32(L::rowbar(g)) + 8 * ((G - 1) & 1), (uint32_t)((G - 1) >> 1) & 1u);
+      band4_flush<NN, NAPP, SITE>(g, T, P);
+      if (i + kPref4 + 1 <= P.last_rho) band4_load_row(a, g, T, P, i + kPref4 + 1, bars);
+    }
     smem4[L::xl(g, 0, buf) + T.p] = nt.c[0];
     smem4[L::xr(g, 0, buf) + T.p] = nt.c[kCols - 1];
     if constexpr (NAPP >= 2) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 2>(a, g, T, P, R, i, j);
@@ -546,6 +579,7 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
       }
     }
   }
+  if constexpr (SPLIT) mbar_arrive4(smem_u32(L::rowbar(g)) + 8 * ((P.g0 + i) & 1));
 }
 
 template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int DG>
@@ -590,8 +624,13 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
   const uint32_t bars = smem_u32(L::bars(g));
   if (NN > 0 && p == 0) {
     for (int q = 0; q < kRing4; ++q) mbar_init(bars + 8 * q, 1);
+    if (band4_split<NN>()) {
+      mbar_init(smem_u32(L::rowbar(g)), NP);
+      mbar_init(smem_u32(L::rowbar(g)) + 8, NP);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  int g0 = 0;
 
   // this CTA's contiguous run of norm blocks
   const int64_t G = gridDim.x;
@@ -636,6 +675,7 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
     P.dst = a.psi_out + r * dim;
     P.part = a.partial + r * nblk;
     P.pend = -1;
+    P.g0 = g0;
     P.grow0 = r * n;
     P.ph = &ph_bits;
     P.j0 = P.ya - NAPP + 1;                    // first iteration's stage-1 row
@@ -672,6 +712,7 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
     } else {
       band4_loop<NN, NAPP, RK4, SITE, EXACT, true, DG>(a, g, T, P, R, iters, bars);
     }
+    g0 += (iters + 2) / 3 * 3;  // the loop runs whole groups of three iterations
     if constexpr (NN == 0) cpa_wait<0>();
     __syncthreads();
     band4_flush<NN, NAPP, SITE>(g, T, P);

@@ -17,7 +17,7 @@ Band4Plan plan_band4(int n, int napp, bool site, int64_t count) {
   const int nx = napp > 1 ? napp - 1 : 1;
   p.smem = (size_t)kRing4 * p.npad * sizeof(double2) + (size_t)nx * 4 * p.threads * sizeof(double2) +
            (size_t)n * sizeof(double2) + (size_t)((site ? n : 0) + 64 + (site ? 9 : 5) * p.threads) * sizeof(double) +
-           kRing4 * sizeof(uint64_t);
+           (kRing4 + 2) * sizeof(uint64_t);
   if (napp == 4 && (n == 256 || n == 512 || n == 1024) && stash_fits(n, site))
     p.smem += 16 + (size_t)4 * p.threads * sizeof(double2);  // RK4 stash (also sized for Taylor-4: harmless)
   return p;
