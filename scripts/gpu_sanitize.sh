@@ -5,7 +5,7 @@ set -u
 OUT=gpurun_out/${1:-san}
 mkdir -p $OUT
 for tool in memcheck racecheck synccheck; do
-  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize.py resident64 gram points band4 \
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize.py ${WHICH:-resident64 gram points band4} \
     > $OUT/$tool.log 2>&1; echo "rc=$?" >> $OUT/$tool.log
   tail -3 $OUT/$tool.log
 done

@@ -63,6 +63,9 @@ if __name__ == "__main__":
     if "band4" in which:
         run(2, 96, 3, 3)
         run(2, 256, 2, 2, "rk4")
+    if "band4split" in which:  # N = 1024: the split-phase row barrier
+        run(2, 1024, 2, 2)
+        run(2, 1024, 2, 2, "rk4")
     if "resident" in which:
         run(2, 32, 3, 4)
     if "generic" in which:
