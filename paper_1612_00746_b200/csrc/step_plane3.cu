@@ -119,7 +119,8 @@ constexpr int kHaloOff = kXOff + 3 * kXStage;
 constexpr int kHopOff = kHaloOff + 3 * 2 * 2 * kN3;
 constexpr int kSiteOff = kHopOff + kN3;          // doubles follow, in double2 units of the base
 constexpr int kBars3 = kRing3 + 6;               // ring slots, halo "full" [3 stages][2 parity]
-constexpr size_t kSmem3 = (size_t)(kSiteOff) * 16 + (size_t)kN3 * 8 + 16 * 8 + kBars3 * 8;
+constexpr int kSplit3 = kBars3;                   // + split-phase plane barrier [iteration parity]
+constexpr size_t kSmem3 = (size_t)(kSiteOff) * 16 + (size_t)kN3 * 8 + 16 * 8 + (kBars3 + 2) * 8;
 
 __device__ __forceinline__ double* site_tab() { return reinterpret_cast<double*>(smem3 + kSiteOff); }
 __device__ __forceinline__ double* red_tab() { return site_tab() + kN3; }
@@ -160,6 +161,7 @@ struct Piece3 {
   bool scale;
   int pend, pend2;
   int iters;  // iterations the loop executes (phase-unrolled by 3); the last pushes nothing
+  int it0;    // CTA iteration count before this piece (split barrier phases)
   uint32_t* ph;
 };
 
@@ -504,24 +506,10 @@ template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD, bool SC, int PH>
 __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i) {
   const int j = P.j0 + i;
   wait_plane(P, i + 2);
-  // pairs with the arrives at the end of the last iteration: every CTA of
-  // the cluster has consumed the halo rows this iteration overwrites, and
-  // (through the CTA barrier inside the arrive) this CTA's exchange rows and
-  // ring reads of the last iteration are published / retired
-  if (i > 0) cluster_wait();
-  // The wait pairs with arrives made before this thread's (and every other
-  // thread's) wait_plane above, so it does not order the rescale writes of
-  // wait_plane; a CTA barrier does.  Only pieces with a pending rescale pay it.
+  // Orders the rescale writes of wait_plane before stage 1 reads the tile
+  // (only pieces with a pending rescale pay it), and starts each piece.
   if (i == 0 || P.scale) __syncthreads();
-  flush3(T, P);
-  if (i + pref3<RK4>() + 1 <= P.last_rho) load_plane(a, T, P, i + pref3<RK4>() + 1);
   const int buf = i & 1;
-  // arm the barriers that count this iteration's incoming halo pushes (their
-  // previous phase, iteration i-2's pushes, was awaited by warp 0 last iteration)
-  if (i < P.iters - 1 && threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) mbar_arm3(full_bar(k, buf), 2 * kN3 * 16);
-  }
   constexpr double c16 = 1.0 / 6.0;
   constexpr int SM1 = (PH + 2) % 3;
   const int r = wrap3(j);
@@ -557,6 +545,26 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
     for (int q = 0; q < 4; ++q) R.acc[SM1].c[q] = cadd(R.up.c[q], mid1.c[q]);
     nt = t;
   }
+  // Split-phase synchronisation: stage 1 above read only this CTA's ring.
+  // Before anything is published: every thread of the CTA has finished the
+  // last iteration (its exchange rows are visible, its ring and exchange
+  // reads retired, its norm partials written: the arrive at the end of the
+  // iteration, an mbarrier per iteration parity), and every CTA of the
+  // cluster has consumed the halo rows this iteration's pushes overwrite
+  // (the relaxed cluster barrier).
+  if (i > 0) {
+    const int G = P.it0 + i - 1;
+    mbar_wait3(bar_addr(kSplit3 + (G & 1)), (uint32_t)(G >> 1) & 1u);
+    cluster_wait();
+  }
+  flush3(T, P);
+  if (i + pref3<RK4>() + 1 <= P.last_rho) load_plane(a, T, P, i + pref3<RK4>() + 1);
+  // arm the barriers that count this iteration's incoming halo pushes (their
+  // previous phase, iteration i-2's pushes, was awaited last iteration)
+  if (i < P.iters - 1 && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mbar_arm3(full_bar(k, buf), 2 * kN3 * 16);
+  }
   xch_put(T, 0, buf, nt);
   if (i < P.iters - 1) halo_push(T, 0, buf, nt);
   R.m1 = nt;
@@ -569,7 +577,9 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, NAPP>(a, T, P, R, i, j, xch_own(T, NAPP - 2, buf ^ 1), t3,
                                                      xch_nb(T, NAPP - 2, buf ^ 1));
   if (RK4) R.acc[PH] = t;
-  cluster_arrive();
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_addr(kSplit3 + ((P.it0 + i) & 1)))
+               : "memory");
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 }
 
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD, bool SC>
@@ -608,8 +618,11 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
   if (threadIdx.x == 0) {
     for (int q = 0; q < kBars3; ++q)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_addr(q)), "r"(1) : "memory");
+    for (int q = 0; q < 2; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_addr(kSplit3 + q)), "r"(kThreads3) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  int it0 = 0;
   // the cluster's run of (realization, x0 block) work items; in place, whole
   // realizations only (a split realization would overwrite another piece's halo)
   const int64_t nclus = gridDim.x / kCl;
@@ -657,6 +670,8 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     P.j0 = P.ya - NAPP + 1;
     const int iters = (P.yb - P.ya) + 2 * (NAPP - 1);
     P.iters = (iters + 2) / 3 * 3;
+    P.it0 = it0;
+    it0 += P.iters;
     P.last_rho = iters + 1;
     for (int rho = 0; rho <= pref3<RK4>(); ++rho)
       if (rho <= P.last_rho) load_plane(a, T, P, rho);
