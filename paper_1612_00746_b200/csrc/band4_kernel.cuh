@@ -363,7 +363,7 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   constexpr bool RKF = rk4fma<RK4, EXACT>();
   const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[NAPP - K] : a.ci[K - 1]);
   Row4 tk;
-  apply4<EXACT, SITE, DG, !RK4, HORN, RKF>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0,
+  apply4<EXACT, SITE, DG, !RK4 || RKF, HORN, RKF>(T, a.k, rr, smem4[L::hop2(g) + rr], SITE ? L::site(g)[rr] : 0.0,
                                            R.w[K - 1][sm], R.w[K - 1][s0], R.w[K - 1][sp], lf, rt, ci, tk,
                                            &R.acc[s0]);
   if constexpr (RKF) {
@@ -509,7 +509,7 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
   constexpr bool HORN = horner4<NAPP, RK4, EXACT>();
   constexpr bool RKF = rk4fma<RK4, EXACT>();
   Row4 t;
-  apply4<EXACT, SITE, DG, !RK4, HORN, RKF>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, psi,
+  apply4<EXACT, SITE, DG, !RK4 || RKF, HORN, RKF>(T, a.k, r, smem4[L::hop2(g) + r], SITE ? L::site(g)[r] : 0.0, R.up, psi,
                                            dn, lf, rt, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
   if constexpr (NAPP == 1) {
     Row4 o;
