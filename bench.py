@@ -486,20 +486,11 @@ def enqueue_schedule(engine, cfg, ens, first, steps, torch, group=None):
     (engine._fused_groups: ctqw_evolve_observe per group of points, one
     all-reduce of the point limbs, ctqw_observe_points).  Returns the last
     group's (out, diag) device buffers."""
-    from paper_1612_00746_b200 import sharding
-
-    n, dim = cfg.space.lattice.n_sites, cfg.space.dim
     out = diag = None
     for start, targets in engine._fused_groups(cfg):
         if targets[-1] > steps:
             break
-        npts = len(targets)
-        acc = torch.empty((npts, 3, dim), dtype=torch.int64, device=ens.dev)
-        ens.evolve_observe(first + start, targets[-1] - start, cfg.post_rate, acc)
-        sharding.allreduce_sum_(acc, group)
-        out = torch.empty((npts, n + 3), dtype=torch.float64, device=ens.dev)
-        diag = torch.empty((npts, dim), dtype=torch.float64, device=ens.dev)
-        ens.handle.observe_points(acc, npts, float(cfg.realizations), out, diag)
+        out, diag, _ = engine.enqueue_group(cfg, ens, first + start, [first + t for t in targets], group)
     return out, diag
 
 

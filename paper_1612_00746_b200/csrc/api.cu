@@ -713,7 +713,7 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
 
 int ctqw_evolve_observe(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t count, int64_t first_step,
                         int64_t n_steps, int64_t post_rate, int64_t* acc_dev, const ctqw_stepper_t* st,
-                        int32_t* result_in_work, void* stream) {
+                        int32_t keep_stats, int32_t* result_in_work, void* stream) {
   if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
   int rc = validate_stepper(h, st);
   if (rc) return rc;
@@ -735,7 +735,7 @@ int ctqw_evolve_observe(ctqw_handle_t h, double* psi_dev, double* work_dev, int6
     o.post_rate = post_rate;
     o.origin = first_step;
     o.final_step = last;
-    return evolve_impl(h, psi_dev, work_dev, count, first_step, n_steps, st, result_in_work, s, true, o);
+    return evolve_impl(h, psi_dev, work_dev, count, first_step, n_steps, st, result_in_work, s, !keep_stats, o);
   }
   // every other path: one segment per collection point, then the separate
   // exact-limb pass over the state (the same bits as the fused form)
@@ -745,7 +745,8 @@ int ctqw_evolve_observe(ctqw_handle_t h, double* psi_dev, double* work_dev, int6
   for (int64_t idx = 0; idx < npoints; ++idx) {
     const int64_t target = std::min<int64_t>(last, first_step + (idx + 1) * post_rate);
     int32_t swapped = 0;
-    rc = evolve_impl(h, cur, other, count, done, target - done, st, &swapped, s, idx == 0, ObsTarget{});
+    rc = evolve_impl(h, cur, other, count, done, target - done, st, &swapped, s, idx == 0 && !keep_stats,
+                     ObsTarget{});
     if (rc) return rc;
     if (swapped) std::swap(cur, other);
     done = target;

@@ -434,7 +434,7 @@ class EnsembleState:
         if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
 
-    def evolve_observe(self, first_step: int, n_steps: int, post_rate: int, acc):
+    def evolve_observe(self, first_step: int, n_steps: int, post_rate: int, acc, keep_stats: bool = False):
         """Enqueue ``n_steps`` steps and the collection points among them
         (every ``post_rate``-th step from ``first_step``, and the last one): acc[P][3][D]
         int64 receives each point's exact limbs of sum_r |psi_r|^2
@@ -444,7 +444,7 @@ class EnsembleState:
             acc.zero_()
             return
         swapped = self.handle.evolve_observe(self.psi, self.work, self.count, first_step, n_steps, post_rate, acc,
-                                             self.stepper)
+                                             self.stepper, keep_stats)
         if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
 
@@ -613,10 +613,12 @@ FUSED_ACC_BYTES = 512 * 2**20
 def fused_collection_ok(config: RunConfig, sinks, world: int) -> bool:
     """run() takes the batched path (ctqw_evolve_observe + ctqw_observe_points:
     one call per group of collection points instead of a segment call, a
-    limb pass and four reductions per point) unless a point needs the states
-    themselves (purity, the dense rho) or the run is sharded."""
-    return (world == 1 and OBS_PURITY not in config.observables and not getattr(sinks, "dense_density", False)
-            and config.steps > 0)
+    limb pass and four reductions per point, and one host synchronisation
+    per group) unless the sink wants the dense rho or the run is sharded.
+    With purity, which needs the states at every point, the group issues one
+    evolve_observe per segment plus the overlap kernel, still without a host
+    synchronisation per point."""
+    return world == 1 and not getattr(sinks, "dense_density", False) and config.steps > 0
 
 
 def _fused_groups(config: RunConfig):
@@ -634,6 +636,36 @@ def _fused_groups(config: RunConfig):
     return groups
 
 
+def enqueue_group(config: RunConfig, ens, start: int, targets, group=None):
+    """Enqueue one group of collection points on the batched path (no host
+    synchronisation): the steps from ``start`` to ``targets[-1]`` with the
+    exact diag limbs at every target (ctqw_evolve_observe; per segment, with
+    the overlap kernel, when purity is requested), one all-reduce of the
+    limbs, and ctqw_observe_points.  Returns device buffers (out[P][N+3],
+    diag[P][D], purity sums[P] or None)."""
+    import torch
+
+    n, dim = config.space.lattice.n_sites, config.space.dim
+    npts = len(targets)
+    acc = torch.empty((npts, 3, dim), dtype=torch.int64, device=ens.dev)
+    pur = None
+    if OBS_PURITY in config.observables:
+        pur = torch.empty(npts, dtype=torch.float64, device=ens.dev)
+        prev = start
+        for k, t in enumerate(targets):
+            ens.evolve_observe(prev, t - prev, t - prev, acc[k:k + 1], keep_stats=k > 0)
+            st = sharding.gather_states(ens.states(), group)
+            ens.handle.overlap_sumsq(st, st.shape[0], st, st.shape[0], pur[k:k + 1])
+            prev = t
+    else:
+        ens.evolve_observe(start, targets[-1] - start, config.post_rate, acc)
+    sharding.allreduce_sum_(acc, group)
+    out = torch.empty((npts, n + 3), dtype=torch.float64, device=ens.dev)
+    diag = torch.empty((npts, dim), dtype=torch.float64, device=ens.dev)
+    ens.handle.observe_points(acc, npts, float(config.realizations), out, diag)
+    return out, diag, pur
+
+
 def _run_fused(config, ens, sinks, emit, profile, clock):
     """The schedule loop of run() on the batched path; same rows, events,
     counters and failure semantics as the per-segment loop."""
@@ -642,17 +674,14 @@ def _run_fused(config, ens, sinks, emit, profile, clock):
     n = config.space.lattice.n_sites
     dim = config.space.dim
     want_joint = OBS_JOINT in config.observables
+    want_purity = OBS_PURITY in config.observables
     totals = {"corrections": 0, "events": 0, "max_dev": 0.0, "snapshots": 0}
     for start, targets in _fused_groups(config):
-        npts = len(targets)
         t0 = clock()
-        acc = torch.empty((npts, 3, dim), dtype=torch.int64, device=ens.dev)
-        ens.evolve_observe(start, targets[-1] - start, config.post_rate, acc)
-        out = torch.empty((npts, n + 3), dtype=torch.float64, device=ens.dev)
-        diag = torch.empty((npts, dim), dtype=torch.float64, device=ens.dev)
-        ens.handle.observe_points(acc, npts, float(config.realizations), out, diag)
+        out, diag, pur = enqueue_group(config, ens, start, targets)
         local = ens.stats()  # synchronises
         host = out.cpu().numpy()
+        pur_host = pur.cpu().numpy() if pur is not None else None
         profile.add(STAGE_EVOLUTION, clock() - t0, calls=config.realizations * (targets[-1] - start))
         profile.add(STAGE_HAMILTONIAN, 0.0, calls=config.realizations * (targets[-1] - start))
         fail = local["failure"]
@@ -678,9 +707,10 @@ def _run_fused(config, ens, sinks, emit, profile, clock):
                 # not torch's reciprocal multiply)
                 joint = diag[k].cpu().numpy() / float(config.realizations) if want_joint else None
                 time_tag = target * config.stepper.dt
-                rows = _observable_rows(config, pops, pr, None, joint)
+                purity = float(pur_host[k]) / float(config.realizations) ** 2 if want_purity else None
+                rows = _observable_rows(config, pops, pr, purity, joint)
                 rho = DiagonalDensity(diag=None, dim=dim, sample_count=config.realizations,
-                                      time_tag=float(time_tag), purity=None, populations=pops,
+                                      time_tag=float(time_tag), purity=purity, populations=pops,
                                       participation_ratio=pr, device_diag=diag[k])
             totals["snapshots"] += 1
             emit(sinks.observable_rows, rho.time_tag, rows)

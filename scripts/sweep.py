@@ -28,8 +28,8 @@ ONLY = ""
 def timed(ens, cfg, steps, post_rate, engine, torch):
     """Device seconds of ``steps`` steps with a collection point every
     ``post_rate`` steps, the way run() schedules them: the batched path
-    (ctqw_evolve_observe + ctqw_observe_points, bench.enqueue_schedule), or
-    per segment when purity (which needs the states) is requested."""
+    (ctqw_evolve_observe + ctqw_observe_points, bench.enqueue_schedule;
+    with purity, one evolve_observe per segment plus the overlap kernel)."""
     import dataclasses
 
     import bench
@@ -39,15 +39,7 @@ def timed(ens, cfg, steps, post_rate, engine, torch):
     stop = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     start.record()
-    if engine.OBS_PURITY in c.observables:
-        done = 0
-        while done < steps:
-            span = min(post_rate, steps - done)
-            ens.evolve(done, span)
-            done += span
-            engine.collect_observables(c, ens)
-    else:
-        bench.enqueue_schedule(engine, c, ens, 0, steps, torch)
+    bench.enqueue_schedule(engine, c, ens, 0, steps, torch)
     stop.record()
     torch.cuda.synchronize()
     st = ens.stats()

@@ -92,6 +92,8 @@ def _run(p, cfg, fused, monkeypatch):
     (64, 60, 7, 0.11, ("populations", "participation_ratio", "joint_distribution")),  # rescales, ragged
     (96, 40, 15, 0.05, None),                        # band/tile path, segment loop
     (64, 30, 10, 0.35, None),                        # norm failure mid-run
+    (64, 100, 10, 0.02, ("populations", "position_mean_variance", "purity", "participation_ratio")),  # purity
+    (64, 45, 7, 0.11, ("purity", "joint_distribution")),  # purity with renormalisations, ragged schedule
 ])
 def test_run_batched_path_equals_segment_path(pkg, monkeypatch, n, steps, post, dt, obs):
     p = pkg
