@@ -165,6 +165,15 @@ int ctqw_bind_coefficients(ctqw_handle_t h, int64_t count, const double *hop_dev
 int ctqw_fill_states(ctqw_handle_t h, double *psi_dev, int64_t count, const double *psi0_dev,
                      void *stream);
 
+/* Lazy form of ctqw_fill_states (ensemble.py:678, np.tile(psi0)): the next
+ * ctqw_evolve / ctqw_evolve_observe on this handle starts every realization
+ * from psi0_dev (one state, D complex128, kept alive by the caller until
+ * then) without writing the R x D stack first -- the band4 and resident64
+ * kernels read it directly in the first step; other paths fill the stack
+ * themselves.  Until that call the contents of psi are undefined (call
+ * ctqw_fill_states to materialise them); ctqw_fill_states cancels it. */
+int ctqw_set_initial(ctqw_handle_t h, const double *psi0_dev);
+
 /* out = H psi for a batch (apply_values, hamiltonian.py:195-223). */
 int ctqw_apply(ctqw_handle_t h, const double *psi_dev, double *out_dev, int64_t count,
                int32_t exact, void *stream);

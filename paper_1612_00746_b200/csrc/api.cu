@@ -62,6 +62,7 @@ struct ctqw_ctx {
   int64_t fixed_cap = 0;
   double* overlap_partial = nullptr;
   int64_t overlap_cap = 0;
+  const double2* initial = nullptr;  // ctqw_set_initial: the next evolve starts every realization from this state
   double* points_scratch = nullptr;  // ctqw_observe_points: per-point partials (+ diag when the caller gives none)
   int64_t points_cap = 0;
   int64_t last_count = 0;
@@ -575,6 +576,13 @@ int ctqw_fill_states(ctqw_handle_t h, double* psi_dev, int64_t count, const doub
   CUDA_TRY(h, launch_fill_states((double2*)psi_dev, count, h->dim, (const double2*)psi0_dev,
                                  (cudaStream_t)stream));
   h->launches += 1;
+  h->initial = nullptr;
+  return CTQW_OK;
+}
+
+int ctqw_set_initial(ctqw_handle_t h, const double* psi0_dev) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  h->initial = (const double2*)psi0_dev;
   return CTQW_OK;
 }
 
@@ -773,7 +781,14 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
     CUDA_TRY(h, launch_reset_stats(h->stats, h->scl, count, h->fail, s));
     h->launches += 1;
   }
-  if (count == 0 || n_steps == 0) return CTQW_OK;
+  if (count == 0 || n_steps == 0) {
+    if (h->initial && count > 0) {  // nothing to step: the stack is the initial state
+      CUDA_TRY(h, launch_fill_states((double2*)psi_dev, count, h->dim, h->initial, s));
+      h->launches += 1;
+    }
+    h->initial = nullptr;
+    return CTQW_OK;
+  }
   const StepScalars sc = scalars_for(h, st);
   const NormPolicy pol{st->tol_norm, st->tol_fail, st->renormalize};
   const bool exact = st->exact != 0;
@@ -792,13 +807,23 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
     std::snprintf(h->variant, sizeof(h->variant), "%s<%s,order=%d,site=%d,exact=%d,N=%d>", h->stream_kernel,
                   sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", sc.order, coef.site != nullptr ? 1 : 0,
                   exact ? 1 : 0, h->n);
+    // a pending initial state: resident64 reads it directly, the strip kernel
+    // needs the stack materialised
+    const double2* init = h->initial;
+    h->initial = nullptr;
+    if (init && !r64) {
+      CUDA_TRY(h, launch_fill_states(psi, count, h->dim, init, s));
+      h->launches += 1;
+      init = nullptr;
+    }
     // dynamic noise changes the couplings after every step: one step per launch
     const int64_t chunk = h->tg_enabled ? 1 : n_steps;
     for (int64_t j = 0; j < n_steps; j += chunk) {
       timing_event(h, s);
       if (r64)
         CUDA_TRY(h, launch_resident64(psi, count, coef, h->k, sc, exact, pol, first_step + j, chunk, h->stats,
-                                      h->events, h->fail, s, obs.acc, obs.post_rate, obs.origin, obs.final_step));
+                                      h->events, h->fail, s, obs.acc, obs.post_rate, obs.origin, obs.final_step,
+                                      j == 0 ? init : nullptr));
       else
         CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step + j, chunk,
                                     h->stats, h->events, h->fail, s));
@@ -855,17 +880,27 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
                                   : tile_parts(h->n, sc);
     rc = ensure(h, &h->partial, &h->partial_cap, count * nparts, "norm partials");
     if (rc) return rc;
+    // a pending initial state: band4's first step reads it as one shared
+    // input (no materialised stack); plane3 (in place) and tile need the stack
+    const double2* init = h->initial;
+    h->initial = nullptr;
+    if (init && !use_band4) {
+      CUDA_TRY(h, launch_fill_states(psi, count, h->dim, init, s));
+      h->launches += 1;
+      init = nullptr;
+    }
     // plane3 marches in place (output planes 0..3 parked until the march ends)
     double2* bufs[2] = {psi, use_plane3 ? psi : work};
     for (int64_t j = 0; j < n_steps; ++j) {
-      const double2* in = bufs[j & 1];
+      const bool from_init = j == 0 && init != nullptr;
+      const double2* in = from_init ? init : bufs[j & 1];
       double2* out = bufs[(j + 1) & 1];
       timing_event(h, s);
       if (use_plane3)
         CUDA_TRY(h, launch_plane3_step(in, out, count, coef, h->k, sc, exact, h->scl, h->partial, h->fail, s));
       else if (use_band4)
         CUDA_TRY(h, launch_band4_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
-                                      h->fail, s));
+                                      h->fail, s, from_init));
       else
         CUDA_TRY(h, launch_tile_step(in, out, count, h->n, coef, h->k, sc, exact, h->scl, h->partial,
                                      h->fail, s));
@@ -887,6 +922,11 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
     h->launches += 2;
     if (result_in_work) *result_in_work = final_buf == psi ? 0 : 1;
     return CTQW_OK;
+  }
+  if (h->initial) {  // the generic kernels step the stack in place
+    CUDA_TRY(h, launch_fill_states(psi, count, h->dim, h->initial, s));
+    h->launches += 1;
+    h->initial = nullptr;
   }
   // generic path: in place on psi; work = term buffer A, library scratch B, C
   h->stream_kernel = sc.backend == CTQW_BACKEND_TAYLOR ? "taylor_order_kernel" : "rk4_stage_kernel";

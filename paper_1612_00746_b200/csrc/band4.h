@@ -36,6 +36,7 @@ struct Band4Args {
   const double* scl;
   double* partial;
   const long long* fail;
+  int bcast;          // psi_in is one state shared by every realization
 };
 
 struct Band4Plan {

@@ -671,12 +671,12 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
     }
     P.s = a.scl ? a.scl[r] : 1.0;
     P.scale = P.s != 1.0;
-    P.src = a.psi_in + r * dim;
+    P.src = a.psi_in + (a.bcast ? 0 : r * dim);
     P.dst = a.psi_out + r * dim;
     P.part = a.partial + r * nblk;
     P.pend = -1;
     P.g0 = g0;
-    P.grow0 = r * n;
+    P.grow0 = a.bcast ? 0 : r * n;
     P.ph = &ph_bits;
     P.j0 = P.ya - NAPP + 1;                    // first iteration's stage-1 row
     const int iters = (P.yb - P.ya) + 2 * (NAPP - 1);
@@ -771,7 +771,7 @@ cudaError_t launch_b4(const Band4Args& args, Band4Plan p, cudaStream_t s) {
   const int64_t grid = std::min<int64_t>(slots, args.count * p.nblk);
   if constexpr (NN > 0) {
     Band4Args a = args;
-    e = encode_rows_map(&a.tmap, a.psi_in, NN, a.count);
+    e = encode_rows_map(&a.tmap, a.psi_in, NN, a.bcast ? 1 : a.count);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)grid, p.threads, p.smem, s>>>(a);
   } else {

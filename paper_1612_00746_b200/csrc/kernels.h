@@ -105,7 +105,7 @@ cudaError_t launch_resident64(double2* psi, int64_t count, const Coef& coef, con
                               const StepScalars& sc, bool exact, const NormPolicy& pol, long long first_step,
                               long long n_steps, RealStat* stats, EventRec* events, long long* fail,
                               cudaStream_t s, unsigned long long* obs = nullptr, long long post_rate = 1,
-                              long long origin = 0, long long final_step = 0);
+                              long long origin = 0, long long final_step = 0, const double2* psi0 = nullptr);
 // Batched post-processing of P collection points from their exact limbs
 // acc[P][3][dim]: diag[P][dim] (scratch or the caller's), out[P][n + 3] =
 // populations (n) + {sum p, sum p^2, participation ratio}.
@@ -127,10 +127,12 @@ cudaError_t launch_plane3_step(const double2* psi_in, double2* psi_out, int64_t 
 // pipeline, persistent row-block schedule; the default streaming path)
 bool band4_supported(int m, int n, const StepScalars& sc);
 int band4_parts(int n);
+// bcast_in: psi_in is ONE state, the input of every realization (the first
+// step from the initial state, without materialising the stack)
 cudaError_t launch_band4_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
                               const Coef& coef, const StencilConst& k, const StepScalars& sc,
                               bool exact, const double* scl, double* partial,
-                              const long long* fail, cudaStream_t s);
+                              const long long* fail, cudaStream_t s, bool bcast_in = false);
 cudaError_t launch_resident(double2* psi, int64_t count, int n, const Coef& coef,
                             const StencilConst& k, const StepScalars& sc, bool exact,
                             const NormPolicy& pol, long long first_step, long long n_steps,

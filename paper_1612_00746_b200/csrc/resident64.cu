@@ -48,6 +48,7 @@ struct Res64Args {
   // fused collection (ctqw_evolve_observe): at every global step g with
   // (g - origin) % post_rate == 0 or g == final_step, the exact limbs of
   // |psi_r(g)|^2 are added into obs[idx][3][N^2], idx = ceil((g - origin) / post_rate) - 1
+  const double2* psi0;  // non-null: every realization starts from this one state
   unsigned long long* obs;
   long long post_rate;
   long long origin;
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
   for (int i = 0; i < kB64; ++i)
 #pragma unroll
     for (int q = 0; q < kB64; ++q) {
-      cur[i][q] = gpsi[(y0 + i) * kN64 + x0 + q];
+      cur[i][q] = (a.psi0 ? a.psi0 : gpsi)[(y0 + i) * kN64 + x0 + q];
       acc[i][q] = cur[i][q];
       if (rim(i, q)) zb[0][zo(y0 + i, x0 + q)] = cur[i][q];
       if (RK4) psis[zo(y0 + i, x0 + q)] = cur[i][q];
@@ -308,8 +309,9 @@ cudaError_t launch_resident64(double2* psi, int64_t count, const Coef& coef, con
                               const StepScalars& sc, bool exact, const NormPolicy& pol, long long first_step,
                               long long n_steps, RealStat* stats, EventRec* events, long long* fail,
                               cudaStream_t s, unsigned long long* obs, long long post_rate, long long origin,
-                              long long final_step) {
+                              long long final_step, const double2* psi0) {
   Res64Args a;
+  a.psi0 = psi0;
   a.obs = obs;
   a.post_rate = post_rate > 0 ? post_rate : 1;
   a.origin = origin;

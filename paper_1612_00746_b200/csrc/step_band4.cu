@@ -74,7 +74,7 @@ int band4_parts(int n) { return (n % kRB == 0) ? n / kRB : 1; }
 cudaError_t launch_band4_step(const double2* psi_in, double2* psi_out, int64_t count, int n,
                               const Coef& coef, const StencilConst& k, const StepScalars& sc,
                               bool exact, const double* scl, double* partial,
-                              const long long* fail, cudaStream_t s) {
+                              const long long* fail, cudaStream_t s, bool bcast_in) {
   const bool site = coef.site != nullptr;
   const int napp = sc.backend == 1 ? 4 : sc.order;
   const Band4Plan p = plan_band4(n, napp, site, count);
@@ -97,6 +97,7 @@ cudaError_t launch_band4_step(const double2* psi_in, double2* psi_out, int64_t c
   a.scl = scl;
   a.partial = partial;
   a.fail = fail;
+  a.bcast = bcast_in ? 1 : 0;
   if (count == 0) return cudaSuccess;
   // eps0 = U = 0: the diagonal base is zero (no multiply, no coincidence select)
   const bool zd = k.base[0] == 0.0 && k.base[1] == 0.0 && k.base[2] == 0.0 && k.base[3] == 0.0;

@@ -420,17 +420,30 @@ class EnsembleState:
         # one buffer when the step kernel marches in place (the library keeps a
         # second one itself if another path ends up running)
         self.work = self.psi if marches_in_place(config) else torch.empty_like(self.psi)
+        # every realization starts from psi0: handed to the library lazily
+        # (ctqw_set_initial), so the first step reads the one state instead of
+        # a materialised R x D stack; anything that reads the states before
+        # the first step materialises them (_materialise)
+        self._initial_pending = False
         if self.count:
-            self.handle.fill_states(self.psi, self.count, self.psi0)
+            self.handle.set_initial(self.psi0)
+            self._initial_pending = True
         self.stepper = config.stepper.native(config.exact)
+
+    def _materialise(self):
+        if self._initial_pending:
+            self.handle.fill_states(self.psi, self.count, self.psi0)
+            self._initial_pending = False
 
     def evolve(self, first_step: int, n_steps: int):
         """Enqueue ``n_steps`` steps (asynchronous)."""
         if self.count == 0 or n_steps == 0:
+            self._materialise()
             self.handle.evolve(self.psi, self.work, 0, first_step, 0, self.stepper)
             return
         swapped = self.handle.evolve(self.psi, self.work, self.count, first_step, n_steps,
                                      self.stepper)
+        self._initial_pending = False
         if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
 
@@ -445,6 +458,7 @@ class EnsembleState:
             return
         swapped = self.handle.evolve_observe(self.psi, self.work, self.count, first_step, n_steps, post_rate, acc,
                                              self.stepper, keep_stats)
+        self._initial_pending = False
         if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
 
@@ -469,15 +483,18 @@ class EnsembleState:
         return int(sum(self.handle.telegraph_read(self.count)[1]))
 
     def diagonal_sum(self, out):
+        self._materialise()
         self.handle.observe_diag(self.psi, self.count, out, accumulate=False)
         return out
 
     def diagonal_limbs(self, acc):
         """acc[3][D] int64 = exact fixed-point limbs of this shard's sum_r |psi_r|^2."""
+        self._materialise()
         self.handle.observe_diag_fixed(self.psi, self.count, acc, accumulate=False)
         return acc
 
     def states(self):
+        self._materialise()
         return self.psi[: self.count]
 
     def release(self):

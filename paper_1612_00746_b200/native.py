@@ -108,6 +108,7 @@ SIGNATURES = {
     "ctqw_observe_reduce": (ctypes.c_int, [_P, _P, _D, _P, _P, _P, _P]),
     "ctqw_overlap_sumsq": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
     "ctqw_packed_gram": (ctypes.c_int, [_P, _I64, _I64, _D, _P, _I32, _P]),
+    "ctqw_set_initial": (ctypes.c_int, [_P, _P]),
     "ctqw_evolve_observe": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, ctypes.POINTER(Stepper),
                                            _I32, ctypes.POINTER(_I32), _P]),
     "ctqw_segment_events": (ctypes.c_int, [_P, _I64, _I64, _I64, ctypes.POINTER(SegmentStats), _P]),
@@ -319,6 +320,10 @@ class Handle:
                                          int(first_step), int(n_steps), ctypes.byref(stepper),
                                          ctypes.byref(flag), self.stream))
         return bool(flag.value)
+
+    def set_initial(self, psi0):
+        self._initial = psi0  # kept alive until the next evolve reads it
+        self._check(self.lib.ctqw_set_initial(self._h, _ptr(psi0)))
 
     def evolve_observe(self, psi, work, count: int, first_step: int, n_steps: int, post_rate: int, acc,
                        stepper: Stepper, keep_stats: bool = False) -> bool:
