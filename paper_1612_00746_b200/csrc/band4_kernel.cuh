@@ -192,6 +192,7 @@ struct Piece4 {
   bool scale;
   int pend;           // norm block awaiting its flush (-1 none)
   int g0;             // CTA iteration count before this piece (split barrier phases)
+  int pend_it;        // iteration whose last stage completed norm block pend
   int64_t grow0;      // TMA row coordinate of psi row 0 of this realization (r * n)
   uint32_t* ph;       // per-slot mbarrier phase bits (TMA path)
 };
@@ -327,7 +328,7 @@ struct Regs4 {
 // adds the warps in order after the next barrier).
 template <int NN, int NAPP, bool SITE>
 __device__ __forceinline__ void band4_store(const Geo4<NN>& g, const T4& T, Piece4& P, int rr, const Row4& o,
-                                            double& nrm) {
+                                            double& nrm, int it) {
   double2* op = P.dst + (int64_t)rr * g.n() + kCols * T.p;
   st256(op, o.c[0], o.c[1]);
   st256(op + 2, o.c[2], o.c[3]);
@@ -341,15 +342,17 @@ __device__ __forceinline__ void band4_store(const Geo4<NN>& g, const T4& T, Piec
     if ((T.p & 31) == 0) Lay4<NN, NAPP, SITE>::red(g)[(blk & 1) * 32 + (T.p >> 5)] = v;
     nrm = 0.0;
     P.pend = blk;
+    P.pend_it = it;
   }
 }
 
 // Stage K (2..NAPP) of iteration j: row j-K+1 from window K-1 (rows j-K ..
 // j-K+2, slot(y) = (y - j0) mod 3) and the neighbour columns stage K-1
 // published last iteration.
-template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int DG, int PH, int K>
+template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int DG, int PH, int K, bool PRE = false>
 __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& g, const T4& T, Piece4& P,
-                                            Regs4<NAPP>& R, int i, int j) {
+                                            Regs4<NAPP>& R, int i, int j, double2 lf_pre = double2(),
+                                            double2 rt_pre = double2()) {
   using L = Lay4<NN, NAPP, SITE>;
   constexpr double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
   constexpr int s0 = ((PH - K + 1) % 3 + 3) % 3;  // row j-K+1
@@ -357,8 +360,9 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   constexpr int sp = (s0 + 1) % 3;                // row j-K+2
   const int buf = i & 1;
   const int rr = g.wrap(j - K + 1);
-  const double2 lf = smem4[L::xr(g, K - 2, buf ^ 1) + T.pl];
-  const double2 rt = smem4[L::xl(g, K - 2, buf ^ 1) + T.pr];
+  // PRE: the neighbour columns were read before the warp's early arrive
+  const double2 lf = PRE ? lf_pre : smem4[L::xr(g, K - 2, buf ^ 1) + T.pl];
+  const double2 rt = PRE ? rt_pre : smem4[L::xl(g, K - 2, buf ^ 1) + T.pr];
   constexpr bool HORN = horner4<NAPP, RK4, EXACT>();
   constexpr bool RKF = rk4fma<RK4, EXACT>();
   const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[NAPP - K] : a.ci[K - 1]);
@@ -373,7 +377,7 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
       Row4 o;
 #pragma unroll
       for (int q = 0; q < kCols; ++q) o.c[q] = ifma(R.acc[s0].c[q], a.rkw[2], tk.c[q]);
-      if (jo >= P.ya && jo < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, rr, o, R.nrm);
+      if (jo >= P.ya && jo < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, rr, o, R.nrm, i);
     } else {
       // arg = psi(row) + k/2 (K = 2) or + k (K = 3), psi re-read from the ring
       const Row4 pm = ring_row<SC>(g, T, (i + (K == 2 ? 0 : -1)) & (kRing4 - 1), P.s);
@@ -395,7 +399,7 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
 #pragma unroll
     for (int q = 0; q < kCols; ++q)
       o.c[q] = HORN ? tk.c[q] : (RK4 ? cadd(R.acc[s0].c[q], rmul(c16, tk.c[q])) : cadd(R.acc[s0].c[q], tk.c[q]));
-    if (jo >= P.ya && jo < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, rr, o, R.nrm);
+    if (jo >= P.ya && jo < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, rr, o, R.nrm, i);
   } else if constexpr (HORN) {
     R.w[K][s0] = tk;
     smem4[L::xl(g, K - 1, buf) + T.p] = tk.c[0];
@@ -515,7 +519,7 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
     Row4 o;
 #pragma unroll
     for (int q = 0; q < kCols; ++q) o.c[q] = cadd(psi.c[q], t.c[q]);
-    if (j >= P.ya && j < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, r, o, R.nrm);
+    if (j >= P.ya && j < P.yb) band4_store<NN, NAPP, SITE>(g, T, P, r, o, R.nrm, i);
   } else {
     Row4 nt;
     if constexpr (RKF) {
@@ -561,14 +565,32 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
       // TMA refills are no longer read, its norm-block partials are in place
       const int G = P.g0 + i;
       if (i > 0) mbar_wait(smem_u32(L::rowbar(g)) + 8 * ((G - 1) & 1), (uint32_t)((G - 1) >> 1) & 1u);
-      band4_flush<NN, NAPP, SITE>(g, T, P);
+      // the arrives come before the last stage, so a norm block whose last
+      // row was stored in iteration i-1 is complete only at iteration i+1
+      if (P.pend >= 0 && P.pend_it <= i - (SITE ? 2 : 1)) band4_flush<NN, NAPP, SITE>(g, T, P);
       if (i + kPref4 + 1 <= P.last_rho) band4_load_row(a, g, T, P, i + kPref4 + 1, bars);
     }
     smem4[L::xl(g, 0, buf) + T.p] = nt.c[0];
     smem4[L::xr(g, 0, buf) + T.p] = nt.c[kCols - 1];
     if constexpr (NAPP >= 2) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 2>(a, g, T, P, R, i, j);
     if constexpr (NAPP >= 3) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 3>(a, g, T, P, R, i, j);
-    if constexpr (NAPP >= 4) band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 4>(a, g, T, P, R, i, j);
+    if constexpr (NAPP >= 4) {
+      // early arrive: measured +2 % with on-site noise (the headline) and -7 %
+      // without (register allocation of the zero-diagonal variant), so only
+      // the on-site variants use it
+      if constexpr (SPLIT && SITE) {
+        // the last stage publishes nothing and reads neither the ring nor
+        // any exchange row but its two neighbour columns: read those, then
+        // arrive, so the other warps' waits do not cover this stage too (its
+        // norm-block partial is flushed one row later, band4_store)
+        const double2 lf4 = smem4[L::xr(g, NAPP - 2, buf ^ 1) + T.pl];
+        const double2 rt4 = smem4[L::xl(g, NAPP - 2, buf ^ 1) + T.pr];
+        mbar_arrive4(smem_u32(L::rowbar(g)) + 8 * ((P.g0 + i) & 1));
+        band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 4, true>(a, g, T, P, R, i, j, lf4, rt4);
+      } else {
+        band4_stage<NN, NAPP, RK4, SITE, EXACT, SC, DG, PH, 4>(a, g, T, P, R, i, j);
+      }
+    }
     if constexpr (RK4) {
       if constexpr (stash_fits(NN, SITE)) {
         const double2* st = L::stash(g);
@@ -579,7 +601,7 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
       }
     }
   }
-  if constexpr (SPLIT) mbar_arrive4(smem_u32(L::rowbar(g)) + 8 * ((P.g0 + i) & 1));
+  if constexpr (SPLIT && !SITE) mbar_arrive4(smem_u32(L::rowbar(g)) + 8 * ((P.g0 + i) & 1));
 }
 
 template <int NN, int NAPP, bool RK4, bool SITE, bool EXACT, bool SC, int DG>
@@ -675,6 +697,7 @@ __global__ void __launch_bounds__(kMaxThreads4, 1) band4_kernel(const __grid_con
     P.dst = a.psi_out + r * dim;
     P.part = a.partial + r * nblk;
     P.pend = -1;
+    P.pend_it = 0;
     P.g0 = g0;
     P.grow0 = a.bcast ? 0 : r * n;
     P.ph = &ph_bits;
