@@ -501,8 +501,12 @@ class EnsembleState:
         """Give the state buffers and the handle back now (not whenever the
         garbage collector gets to this object): a following run() then
         reuses the memory instead of mapping fresh tens of GiB."""
+        from .hamiltonian import release_private_handle
+
         self.psi = self.work = self.psi0 = self.hop = self.site = None
-        self.handle.close()
+        if self.handle is not None:
+            release_private_handle(self.handle)
+            self.handle = None
 
 
 def _observable_rows(config, pops, pr, purity, joint):

@@ -73,6 +73,25 @@ def handle_for(m, n, onsite, tunneling, interaction, hbar, device=None, lattice=
     return h
 
 
+# Free private handles by model key: an ensemble takes one for its lifetime
+# (exclusive: it binds its own coefficient rows and telegraph process) and
+# gives it back when it is released, so repeated runs do not re-create the
+# handle's device and pinned host buffers (cudaMallocHost / cudaFreeHost per
+# run cost up to tens of milliseconds, and vary).
+_PRIVATE_POOL: dict = {}
+
+
+def release_private_handle(h):
+    """Return a private handle to the pool (EnsembleState.release)."""
+    key = getattr(h, "_pool_key", None)
+    if key is None or not getattr(h, "_h", None):
+        return
+    h.telegraph_enable(False)
+    h.set_initial(None)  # a pending initial state of the released ensemble must not leak into the next
+    h._bound = None
+    _PRIVATE_POOL.setdefault(key, []).append(h)
+
+
 def model_handle(topology, model: CouplingModel, hbar=None, device=None, private: bool = False):
     """Handle for ``topology`` + ``model``: the ring as is, any other lattice
     with its move tables and the tunnelling of each slot's direction
@@ -86,19 +105,28 @@ def model_handle(topology, model: CouplingModel, hbar=None, device=None, private
     from .native import Handle
 
     hb = model.hbar if hbar is None else hbar
+
+    def pooled(key, make):
+        free = _PRIVATE_POOL.get(key)
+        h = free.pop() if free else make()
+        h._pool_key = key
+        return h
+
     if topology.is_ring:
         args = (topology.m, topology.n, model.onsite_energy, model.ring_tunneling(), model.interaction, hb)
         if private:
             dev = torch.cuda.current_device() if device is None else device
-            return Handle(*args, dev)
+            return pooled(("ring",) + tuple(float(a) for a in args) + (int(dev),), lambda: Handle(*args, dev))
         return handle_for(*args, device)
     lat = topology.lattice
     pos, neg, directions = topology.move_tables()
     t_slot = model.tunneling_per_direction(lat.q)[directions]
     if private:
         dev = torch.cuda.current_device() if device is None else device
-        return Handle(topology.m, topology.n, model.onsite_energy, float(t_slot[0]), model.interaction, hb, dev,
-                      lattice=(pos, neg, t_slot))
+        key = ("lattice", topology.m, lat.dims, lat.k_half, lat.boundary, tuple(float(v) for v in t_slot),
+               float(model.onsite_energy), float(model.interaction), float(hb), int(dev))
+        return pooled(key, lambda: Handle(topology.m, topology.n, model.onsite_energy, float(t_slot[0]),
+                                          model.interaction, hb, dev, lattice=(pos, neg, t_slot)))
     key = (lat.dims, lat.k_half, lat.boundary, tuple(float(v) for v in t_slot))
     return handle_for(topology.m, topology.n, model.onsite_energy, float(t_slot[0]), model.interaction, hb,
                       device, lattice=(pos, neg, t_slot), lattice_key=key)
