@@ -262,7 +262,11 @@ def estimate_memory(config: RunConfig, world: int = 1) -> dict:
     if not config.noise.is_static:
         total = k_links + n
         noise_state = r_local * (total * (8 + 8 + 12) + 64)  # values, switch times, due lists, generator
-    density = dim * (24 + 8 + 8)  # int64 limbs, diagonal sum, joint distribution
+    # the collection buffers of one group of points on the batched path
+    # (_fused_groups): int64 limbs [P][3][D] + diagonal [P][D], P points per group
+    points = max(1, min(len(config.schedule), FUSED_ACC_BYTES // (24 * dim),
+                        max(1, FUSED_CALL_STEPS // max(config.post_rate, 1))))
+    density = points * dim * (24 + 8) + dim * 8  # + the joint distribution
     return {
         "joint_dim": dim,
         "itemsize": 16,
