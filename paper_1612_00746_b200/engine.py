@@ -459,6 +459,7 @@ class EnsembleState:
         N = 64 path)."""
         if self.count == 0:
             acc.zero_()
+            self.handle.evolve(self.psi, self.work, 0, first_step, 0, self.stepper)  # empty statistics
             return
         swapped = self.handle.evolve_observe(self.psi, self.work, self.count, first_step, n_steps, post_rate, acc,
                                              self.stepper, keep_stats)
@@ -638,12 +639,13 @@ FUSED_ACC_BYTES = 512 * 2**20
 def fused_collection_ok(config: RunConfig, sinks, world: int) -> bool:
     """run() takes the batched path (ctqw_evolve_observe + ctqw_observe_points:
     one call per group of collection points instead of a segment call, a
-    limb pass and four reductions per point, and one host synchronisation
-    per group) unless the sink wants the dense rho or the run is sharded.
+    limb pass and four reductions per point, one host synchronisation and,
+    sharded, one limb all-reduce plus two statistics all-gathers per group)
+    unless the sink wants the dense rho.
     With purity, which needs the states at every point, the group issues one
     evolve_observe per segment plus the overlap kernel, still without a host
     synchronisation per point."""
-    return world == 1 and not getattr(sinks, "dense_density", False) and config.steps > 0
+    return not getattr(sinks, "dense_density", False) and config.steps > 0
 
 
 def _fused_groups(config: RunConfig):
@@ -691,9 +693,10 @@ def enqueue_group(config: RunConfig, ens, start: int, targets, group=None):
     return out, diag, pur
 
 
-def _run_fused(config, ens, sinks, emit, profile, clock):
+def _run_fused(config, ens, sinks, emit, profile, clock, group=None):
     """The schedule loop of run() on the batched path; same rows, events,
-    counters and failure semantics as the per-segment loop."""
+    counters and failure semantics as the per-segment loop, for any number
+    of ranks."""
     import torch
 
     n = config.space.lattice.n_sites
@@ -703,9 +706,14 @@ def _run_fused(config, ens, sinks, emit, profile, clock):
     totals = {"corrections": 0, "events": 0, "max_dev": 0.0, "snapshots": 0}
     for start, targets in _fused_groups(config):
         t0 = clock()
-        out, diag, pur = enqueue_group(config, ens, start, targets)
-        local = ens.stats()  # synchronises
+        out, diag, pur = enqueue_group(config, ens, start, targets, group)
+        local = sharding.merge_segment_stats(sharding.gather_stats(ens.stats(), group))  # synchronises
         host = out.cpu().numpy()
+        seg_events = None
+        if local["event_count"]:
+            prevs = [start] + list(targets[:-1])
+            seg_events = sharding.gather_segment_events(
+                [ens.segment_events(lo, hi) if ens.count else [] for lo, hi in zip(prevs, targets)], group)
         pur_host = pur.cpu().numpy() if pur is not None else None
         profile.add(STAGE_EVOLUTION, clock() - t0, calls=config.realizations * (targets[-1] - start))
         profile.add(STAGE_HAMILTONIAN, 0.0, calls=config.realizations * (targets[-1] - start))
@@ -718,7 +726,7 @@ def _run_fused(config, ens, sinks, emit, profile, clock):
                                     f"reduce the time step")
                 ens.release()
                 raise NormFailureError(dev, realization=real, step=step)
-            events = ens.segment_events(previous, target) if local["event_count"] else []
+            events = seg_events[k] if seg_events is not None else []
             if events:
                 emit(sinks.norm_events, [NormEvent(deviation=d, corrected=c, realization=r, step=s)
                                          for d, c, r, s in events])
@@ -805,7 +813,7 @@ def run(config: RunConfig, sinks: OutputSinks | None = None, group=None) -> RunR
     fused = fused_collection_ok(config, sinks, world)
     if fused:
         with torch.cuda.device(device):
-            tot = _run_fused(config, ens, sinks, emit, profile, clock)
+            tot = _run_fused(config, ens, sinks, emit, profile, clock, group)
         snapshots, corrections = tot["snapshots"], tot["corrections"]
         event_total, max_deviation = tot["events"], tot["max_dev"]
     with torch.cuda.device(device):

@@ -141,6 +141,43 @@ def gather_stats(local, group=None):
     return [unpack_stats(b.cpu().tolist()) for b in bufs]
 
 
+def gather_segment_events(per_segment, group=None):
+    """Per-segment event lists of a group of collection points, merged over
+    the ranks with ONE all-gather: ``per_segment`` is this rank's list (one
+    entry per segment) of (deviation, corrected, realization, step) lists,
+    each holding the rank's first MAX_EVENTS in (step, realization) order;
+    the result keeps, per segment, the first MAX_EVENTS of the union in that
+    order (merge_segment_stats' rule), so it does not depend on the split."""
+    import torch
+    import torch.distributed as dist
+
+    if not _collective(group):
+        return [sorted(evs, key=lambda e: (e[3], e[2]))[:MAX_EVENTS] for evs in per_segment]
+    P = len(per_segment)
+    rec = torch.zeros((P, 1 + 4 * MAX_EVENTS), dtype=torch.float64)
+    for k, evs in enumerate(per_segment):
+        evs = list(evs)[:MAX_EVENTS]
+        rec[k, 0] = float(len(evs))
+        for e, (dev, corrected, real, step) in enumerate(evs):
+            rec[k, 1 + 4 * e: 5 + 4 * e] = torch.tensor([dev, 1.0 if corrected else 0.0, float(real), float(step)],
+                                                        dtype=torch.float64)
+    dev = _comm_device(group)
+    mine = rec.to(dev)
+    bufs = [torch.empty_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(bufs, mine, group=group)
+    recs = [b.cpu().numpy() for b in bufs]
+    out = []
+    for k in range(P):
+        evs = []
+        for r in recs:
+            for e in range(int(r[k, 0])):
+                dv, corr, real, step = r[k, 1 + 4 * e: 5 + 4 * e]
+                evs.append((float(dv), bool(corr), int(real), int(step)))
+        evs.sort(key=lambda e: (e[3], e[2]))
+        out.append(evs[:MAX_EVENTS])
+    return out
+
+
 def merge_segment_stats(per_rank):
     """Combine per-rank segment statistics independently of how the
     realizations were split.
