@@ -261,12 +261,13 @@ int ctqw_packed_gram(const double *psi_dev, int64_t count, int64_t dim, double s
  * as ctqw_observe_diag_fixed).  On the resident N = 64 path the sum is
  * fused into the step kernel; elsewhere each segment is followed by the
  * limb pass.  Statistics accumulate over the whole call (ctqw_segment_stats,
- * ctqw_segment_events), and over earlier calls too when keep_stats != 0 (a
- * caller that needs the states at each point -- purity -- issues one call per
- * segment and reads the statistics once).  n_steps >= 1, post_rate >= 1. */
+ * ctqw_segment_events), and over earlier calls too when keep_stats != 0.
+ * snap_dev (optional, [points][count][dim] complex128) receives the states
+ * themselves at every point (purity needs them: observables.py:86-91).
+ * n_steps >= 1, post_rate >= 1. */
 int ctqw_evolve_observe(ctqw_handle_t h, double *psi_dev, double *work_dev, int64_t count, int64_t first_step,
-                        int64_t n_steps, int64_t post_rate, int64_t *acc_dev, const ctqw_stepper_t *stepper,
-                        int32_t keep_stats, int32_t *result_in_work, void *stream);
+                        int64_t n_steps, int64_t post_rate, int64_t *acc_dev, double *snap_dev,
+                        const ctqw_stepper_t *stepper, int32_t keep_stats, int32_t *result_in_work, void *stream);
 
 /* The events of the last evolve / evolve_observe call with step in
  * (step_lo, step_hi], first CTQW_MAX_EVENTS in (step, realization) order

@@ -690,6 +690,7 @@ struct ObsTarget {
   long long post_rate = 1;
   long long origin = 0;  // the call's first_step: points at origin + k * post_rate and at final_step
   long long final_step = 0;
+  double2* snap = nullptr;  // optional states at each point [point][count][dim]
 };
 
 // Does this handle's evolve run the N = 64 block kernel (which can fuse the
@@ -720,8 +721,8 @@ int ctqw_evolve(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t coun
 }
 
 int ctqw_evolve_observe(ctqw_handle_t h, double* psi_dev, double* work_dev, int64_t count, int64_t first_step,
-                        int64_t n_steps, int64_t post_rate, int64_t* acc_dev, const ctqw_stepper_t* st,
-                        int32_t keep_stats, int32_t* result_in_work, void* stream) {
+                        int64_t n_steps, int64_t post_rate, int64_t* acc_dev, double* snap_dev,
+                        const ctqw_stepper_t* st, int32_t keep_stats, int32_t* result_in_work, void* stream) {
   if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
   int rc = validate_stepper(h, st);
   if (rc) return rc;
@@ -743,6 +744,7 @@ int ctqw_evolve_observe(ctqw_handle_t h, double* psi_dev, double* work_dev, int6
     o.post_rate = post_rate;
     o.origin = first_step;
     o.final_step = last;
+    o.snap = (double2*)snap_dev;
     return evolve_impl(h, psi_dev, work_dev, count, first_step, n_steps, st, result_in_work, s, !keep_stats, o);
   }
   // every other path: one segment per collection point, then the separate
@@ -762,6 +764,9 @@ int ctqw_evolve_observe(ctqw_handle_t h, double* psi_dev, double* work_dev, int6
                                           reinterpret_cast<unsigned long long*>(acc_dev) + idx * 3 * h->dim, true,
                                           s));
     h->launches += 1;
+    if (snap_dev)
+      CUDA_TRY(h, cudaMemcpyAsync(snap_dev + idx * count * h->dim * 2, cur, (size_t)count * h->dim * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, s));
   }
   if (result_in_work) *result_in_work = cur == psi_dev ? 0 : 1;
   return CTQW_OK;
@@ -823,7 +828,7 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
       if (r64)
         CUDA_TRY(h, launch_resident64(psi, count, coef, h->k, sc, exact, pol, first_step + j, chunk, h->stats,
                                       h->events, h->fail, s, obs.acc, obs.post_rate, obs.origin, obs.final_step,
-                                      j == 0 ? init : nullptr));
+                                      j == 0 ? init : nullptr, obs.snap));
       else
         CUDA_TRY(h, launch_resident(psi, count, h->n, coef, h->k, sc, exact, pol, first_step + j, chunk,
                                     h->stats, h->events, h->fail, s));

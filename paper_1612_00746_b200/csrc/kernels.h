@@ -105,7 +105,8 @@ cudaError_t launch_resident64(double2* psi, int64_t count, const Coef& coef, con
                               const StepScalars& sc, bool exact, const NormPolicy& pol, long long first_step,
                               long long n_steps, RealStat* stats, EventRec* events, long long* fail,
                               cudaStream_t s, unsigned long long* obs = nullptr, long long post_rate = 1,
-                              long long origin = 0, long long final_step = 0, const double2* psi0 = nullptr);
+                              long long origin = 0, long long final_step = 0, const double2* psi0 = nullptr,
+                              double2* snap = nullptr);
 // Batched post-processing of P collection points from their exact limbs
 // acc[P][3][dim]: diag[P][dim] (scratch or the caller's), out[P][n + 3] =
 // populations (n) + {sum p, sum p^2, participation ratio}.

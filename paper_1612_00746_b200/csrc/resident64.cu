@@ -53,6 +53,8 @@ struct Res64Args {
   long long post_rate;
   long long origin;
   long long final_step;
+  double2* snap;        // optional: the states at each point, [point][count][N^2] (purity)
+  int64_t count;
 };
 
 // 16-byte chunk x of row y at x ^ ((x >> 3) & 3): the block-row loads
@@ -249,6 +251,13 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
             atomicAdd(o + kPlane64 + al, (unsigned long long)l1);
             atomicAdd(o + 2 * kPlane64 + al, (unsigned long long)l0);
           }
+        if (a.snap) {
+          double2* sp = a.snap + (idx * a.count + r) * (int64_t)kPlane64;
+#pragma unroll
+          for (int i = 0; i < kB64; ++i)
+#pragma unroll
+            for (int q = 0; q < kB64; ++q) sp[(y0 + i) * kN64 + x0 + q] = cur[i][q];
+        }
       }
     }
   }
@@ -309,9 +318,11 @@ cudaError_t launch_resident64(double2* psi, int64_t count, const Coef& coef, con
                               const StepScalars& sc, bool exact, const NormPolicy& pol, long long first_step,
                               long long n_steps, RealStat* stats, EventRec* events, long long* fail,
                               cudaStream_t s, unsigned long long* obs, long long post_rate, long long origin,
-                              long long final_step, const double2* psi0) {
+                              long long final_step, const double2* psi0, double2* snap) {
   Res64Args a;
   a.psi0 = psi0;
+  a.snap = snap;
+  a.count = count;
   a.obs = obs;
   a.post_rate = post_rate > 0 ? post_rate : 1;
   a.origin = origin;

@@ -267,6 +267,9 @@ def estimate_memory(config: RunConfig, world: int = 1) -> dict:
     points = max(1, min(len(config.schedule), FUSED_ACC_BYTES // (24 * dim),
                         max(1, FUSED_CALL_STEPS // max(config.post_rate, 1))))
     density = points * dim * (24 + 8) + dim * 8  # + the joint distribution
+    if OBS_PURITY in config.observables:  # the states at every point of a group (enqueue_group)
+        snap = points * r_local * dim * 16
+        density += snap if snap <= SNAPSHOT_BYTES else 0
     return {
         "joint_dim": dim,
         "itemsize": 16,
@@ -451,7 +454,8 @@ class EnsembleState:
         if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
 
-    def evolve_observe(self, first_step: int, n_steps: int, post_rate: int, acc, keep_stats: bool = False):
+    def evolve_observe(self, first_step: int, n_steps: int, post_rate: int, acc, keep_stats: bool = False,
+                       snap=None):
         """Enqueue ``n_steps`` steps and the collection points among them
         (every ``post_rate``-th step from ``first_step``, and the last one): acc[P][3][D]
         int64 receives each point's exact limbs of sum_r |psi_r|^2
@@ -462,7 +466,7 @@ class EnsembleState:
             self.handle.evolve(self.psi, self.work, 0, first_step, 0, self.stepper)  # empty statistics
             return
         swapped = self.handle.evolve_observe(self.psi, self.work, self.count, first_step, n_steps, post_rate, acc,
-                                             self.stepper, keep_stats)
+                                             self.stepper, keep_stats, snap)
         self._initial_pending = False
         if swapped and self.work is not self.psi:
             self.psi, self.work = self.work, self.psi
@@ -634,6 +638,7 @@ def collect_observables(config, ens: EnsembleState, group=None, want_joint=None)
 # this many steps every segment's event list can be rebuilt exactly
 FUSED_CALL_STEPS = MAX_EVENTS_PER_SEGMENT
 FUSED_ACC_BYTES = 512 * 2**20
+SNAPSHOT_BYTES = 1024 * 2**20  # states kept per group of points for purity
 
 
 def fused_collection_ok(config: RunConfig, sinks, world: int) -> bool:
@@ -678,12 +683,21 @@ def enqueue_group(config: RunConfig, ens, start: int, targets, group=None):
     pur = None
     if OBS_PURITY in config.observables:
         pur = torch.empty(npts, dtype=torch.float64, device=ens.dev)
-        prev = start
-        for k, t in enumerate(targets):
-            ens.evolve_observe(prev, t - prev, t - prev, acc[k:k + 1], keep_stats=k > 0)
-            st = sharding.gather_states(ens.states(), group)
-            ens.handle.overlap_sumsq(st, st.shape[0], st, st.shape[0], pur[k:k + 1])
-            prev = t
+        if npts * max(ens.count, 1) * dim * 16 <= SNAPSHOT_BYTES and ens.count:
+            # the states at every point written by the same call (the resident
+            # kernel stores them from registers), then one overlap pass per point
+            snap = torch.empty((npts, ens.count, dim), dtype=torch.complex128, device=ens.dev)
+            ens.evolve_observe(start, targets[-1] - start, config.post_rate, acc, snap=snap)
+            for k in range(npts):
+                st = sharding.gather_states(snap[k], group)
+                ens.handle.overlap_sumsq(st, st.shape[0], st, st.shape[0], pur[k:k + 1])
+        else:
+            prev = start
+            for k, t in enumerate(targets):
+                ens.evolve_observe(prev, t - prev, t - prev, acc[k:k + 1], keep_stats=k > 0)
+                st = sharding.gather_states(ens.states(), group)
+                ens.handle.overlap_sumsq(st, st.shape[0], st, st.shape[0], pur[k:k + 1])
+                prev = t
     else:
         ens.evolve_observe(start, targets[-1] - start, config.post_rate, acc)
     sharding.allreduce_sum_(acc, group)

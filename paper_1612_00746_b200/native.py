@@ -109,7 +109,7 @@ SIGNATURES = {
     "ctqw_overlap_sumsq": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
     "ctqw_packed_gram": (ctypes.c_int, [_P, _I64, _I64, _D, _P, _I32, _P]),
     "ctqw_set_initial": (ctypes.c_int, [_P, _P]),
-    "ctqw_evolve_observe": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, ctypes.POINTER(Stepper),
+    "ctqw_evolve_observe": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, ctypes.POINTER(Stepper),
                                            _I32, ctypes.POINTER(_I32), _P]),
     "ctqw_segment_events": (ctypes.c_int, [_P, _I64, _I64, _I64, ctypes.POINTER(SegmentStats), _P]),
     "ctqw_observe_points": (ctypes.c_int, [_P, _P, _I64, _D, _P, _P, _P]),
@@ -326,11 +326,12 @@ class Handle:
         self._check(self.lib.ctqw_set_initial(self._h, _ptr(psi0)))
 
     def evolve_observe(self, psi, work, count: int, first_step: int, n_steps: int, post_rate: int, acc,
-                       stepper: Stepper, keep_stats: bool = False) -> bool:
+                       stepper: Stepper, keep_stats: bool = False, snap=None) -> bool:
         flag = _I32(0)
         self._check(self.lib.ctqw_evolve_observe(self._h, _ptr(psi), _ptr(work), int(count), int(first_step),
-                                                 int(n_steps), int(post_rate), _ptr(acc), ctypes.byref(stepper),
-                                                 int(bool(keep_stats)), ctypes.byref(flag), self.stream))
+                                                 int(n_steps), int(post_rate), _ptr(acc), _ptr(snap),
+                                                 ctypes.byref(stepper), int(bool(keep_stats)), ctypes.byref(flag),
+                                                 self.stream))
         return bool(flag.value)
 
     def segment_events(self, r0: int, step_lo: int, step_hi: int) -> SegmentStats:
