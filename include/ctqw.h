@@ -241,6 +241,16 @@ int ctqw_observe_reduce(ctqw_handle_t h, const double *diag_sum_dev, double tota
 int ctqw_overlap_sumsq(ctqw_handle_t h, const double *a_dev, int64_t count_a,
                        const double *b_dev, int64_t count_b, double *sumsq_dev, void *stream);
 
+/* Purity sums of npoints collection points in one launch set: sumsq_dev[p] =
+ * sum_{i,j} |<a_i|a_j>|^2 over the stack stacks_dev + p * point_stride
+ * (complex elements, >= count * dim when npoints > 1), count states each
+ * (observables.py:86-91 at every point of a schedule group; the snapshots
+ * ctqw_evolve_observe writes).  Same result as npoints ctqw_overlap_sumsq
+ * calls with b == a. */
+int ctqw_overlap_sumsq_points(ctqw_handle_t h, const double *stacks_dev, int64_t count,
+                              int64_t npoints, int64_t point_stride, double *sumsq_dev,
+                              void *stream);
+
 /* Packed ensemble density matrix (replaces the Gram product of
  * ctqw/density.py:91-95, accumulate_density): packed_dev[i(i+1)/2 + j] =
  * scale * sum_r psi_r[i] conj(psi_r[j]) for j <= i, psi_dev an (R, dim)

@@ -1094,6 +1094,24 @@ int ctqw_overlap_sumsq(ctqw_handle_t h, const double* a_dev, int64_t count_a, co
   return CTQW_OK;
 }
 
+int ctqw_overlap_sumsq_points(ctqw_handle_t h, const double* stacks_dev, int64_t count, int64_t npoints,
+                              int64_t point_stride, double* sumsq_dev, void* stream) {
+  if (!h) return fail_with(nullptr, CTQW_ERR_CONFIG, "NULL handle");
+  if (count <= 0) return fail_with(h, CTQW_ERR_CONFIG, "empty state stack");
+  if (npoints <= 0 || npoints > 65535) return fail_with(h, CTQW_ERR_CONFIG, "npoints must be in 1..65535");
+  if (npoints > 1 && point_stride < count * h->dim)
+    return fail_with(h, CTQW_ERR_CONFIG, "point_stride smaller than one state stack");
+  DeviceGuard g(h->device);
+  const int64_t need = overlap_scratch_doubles(count, count, true, h->dim, npoints) + 2;
+  int rc = ensure(h, &h->overlap_partial, &h->overlap_cap, need, "overlap partials");
+  if (rc) return rc;
+  const double2* a = (const double2*)stacks_dev;
+  CUDA_TRY(h, launch_overlap_sumsq(a, count, a, count, h->dim, h->overlap_partial, h->overlap_cap, sumsq_dev,
+                                   (cudaStream_t)stream, npoints, point_stride));
+  h->launches += 3;
+  return CTQW_OK;
+}
+
 int ctqw_packed_gram(const double* psi_dev, int64_t count, int64_t dim, double scale, double* packed_dev,
                      int32_t device, void* stream) {
   if (count <= 0) return fail_with(nullptr, CTQW_ERR_CONFIG, "empty state stack");

@@ -172,10 +172,10 @@ cudaError_t launch_observe_reduce(int m, int n, int64_t dim, const double* diag_
                                   double* scratch, cudaStream_t s);
 cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b, int64_t rb,
                                  int64_t dim, double* scratch, int64_t scratch_cap,
-                                 double* out, cudaStream_t s);
+                                 double* out, cudaStream_t s, int64_t npoints = 1, int64_t pstride = 0);
 cudaError_t launch_packed_gram(const double2* psi, int64_t count, int64_t dim, double scale, double2* packed,
                                cudaStream_t s);
 int64_t overlap_parts(int64_t ra, int64_t rb, bool same);
-int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim);
+int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim, int64_t npoints = 1);
 
 }  // namespace ctqw

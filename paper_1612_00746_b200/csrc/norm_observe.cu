@@ -269,9 +269,14 @@ constexpr int kOK = 16;   // D chunk staged through shared memory
 __global__ void __launch_bounds__(256) overlap_partial_kernel(const double2* __restrict__ a, int64_t ra,
                                                               const double2* __restrict__ b, int64_t rb,
                                                               int64_t dim, int same, int64_t ntj,
-                                                              int64_t kspan, double2* __restrict__ gpart) {
+                                                              int64_t kspan, int64_t pstride,
+                                                              double2* __restrict__ gpart) {
   __shared__ double2 sa[kOK][kOT + 1];
   __shared__ double2 sb[kOK][kOT + 1];
+  // blockIdx.z: collection point (stacks pstride elements apart)
+  a += (int64_t)blockIdx.z * pstride;
+  b += (int64_t)blockIdx.z * pstride;
+  gpart += (int64_t)blockIdx.z * gridDim.x * gridDim.y * 256 * 4;
   const int64_t tile = blockIdx.x;
   const int64_t ti = tile / ntj, tj = tile % ntj;
   const int ks = blockIdx.y;
@@ -313,6 +318,8 @@ __global__ void __launch_bounds__(256) overlap_partial_kernel(const double2* __r
 __global__ void __launch_bounds__(256) overlap_finish_kernel(const double2* __restrict__ gpart, int ksplit,
                                                              int same, int64_t ntj, double* partial) {
   __shared__ double red[32];
+  gpart += (int64_t)blockIdx.y * gridDim.x * ksplit * 256 * 4;
+  partial += (int64_t)blockIdx.y * gridDim.x;
   const int64_t tile = blockIdx.x;
   const int64_t ti = tile / ntj, tj = tile % ntj;
   const int tid = threadIdx.x;
@@ -332,6 +339,8 @@ __global__ void __launch_bounds__(256) overlap_finish_kernel(const double2* __re
 
 __global__ void sum_kernel(const double* __restrict__ partial, int64_t nparts, double* out) {
   __shared__ double red[32];
+  partial += (int64_t)blockIdx.x * nparts;  // one block per collection point
+  out += blockIdx.x;
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < nparts; i += blockDim.x) s += partial[i];
   const double b = block_sum(s, red);
@@ -523,6 +532,8 @@ cudaError_t launch_observe_points(int m, int n, int64_t dim, const unsigned long
   return cudaGetLastError();
 }
 
+// (independent of the number of points, so a point's sum does not depend on
+// how the points are batched)
 static int overlap_ksplit(int64_t ra, int64_t rb, bool same, int64_t dim) {
   const int64_t ti = (ra + kOT - 1) / kOT, tj = (rb + kOT - 1) / kOT;
   const int64_t active = same ? ti * (ti + 1) / 2 : ti * tj;
@@ -539,27 +550,32 @@ int64_t overlap_parts(int64_t ra, int64_t rb, bool same) {
   return ti * tj;
 }
 
-int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim) {
+int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim, int64_t npoints) {
   const int64_t tiles = overlap_parts(ra, rb, same);
-  return tiles + tiles * overlap_ksplit(ra, rb, same, dim) * 256 * 4 * 2;
+  const int64_t per = ((tiles + 1) & ~int64_t(1)) + tiles * overlap_ksplit(ra, rb, same, dim) * 256 * 4 * 2;
+  return per * npoints;
 }
 
+// npoints stacks (a and b each advance pstride elements per point): the
+// P overlap sums in one launch set, grid dimension z = point.
 cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b, int64_t rb,
                                  int64_t dim, double* scratch, int64_t scratch_cap, double* out,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, int64_t npoints, int64_t pstride) {
+  if (npoints < 1 || npoints > 65535) return cudaErrorInvalidValue;
   const bool same = (a == b) && (ra == rb);
   const int64_t ntj = (rb + kOT - 1) / kOT;
   const int64_t tiles = overlap_parts(ra, rb, same);
   const int ks = overlap_ksplit(ra, rb, same, dim);
-  if (overlap_scratch_doubles(ra, rb, same, dim) > scratch_cap) return cudaErrorInvalidValue;
-  double* partial = scratch;
-  double2* gpart = reinterpret_cast<double2*>(scratch + ((tiles + 1) & ~int64_t(1)));
+  if (overlap_scratch_doubles(ra, rb, same, dim, npoints) > scratch_cap) return cudaErrorInvalidValue;
+  double* partial = scratch;  // [P][tiles]
+  double2* gpart = reinterpret_cast<double2*>(scratch + ((tiles * npoints + 1) & ~int64_t(1)));
   int64_t kspan = (dim + ks - 1) / ks;
   kspan = ((kspan + kOK - 1) / kOK) * kOK;
-  overlap_partial_kernel<<<dim3((unsigned)tiles, (unsigned)ks), 256, 0, s>>>(a, ra, b, rb, dim, same ? 1 : 0, ntj,
-                                                                             kspan, gpart);
-  overlap_finish_kernel<<<(unsigned)tiles, 256, 0, s>>>(gpart, ks, same ? 1 : 0, ntj, partial);
-  sum_kernel<<<1, 1024, 0, s>>>(partial, tiles, out);
+  overlap_partial_kernel<<<dim3((unsigned)tiles, (unsigned)ks, (unsigned)npoints), 256, 0, s>>>(
+      a, ra, b, rb, dim, same ? 1 : 0, ntj, kspan, pstride, gpart);
+  overlap_finish_kernel<<<dim3((unsigned)tiles, (unsigned)npoints), 256, 0, s>>>(gpart, ks, same ? 1 : 0, ntj,
+                                                                                 partial);
+  sum_kernel<<<(unsigned)npoints, 1024, 0, s>>>(partial, tiles, out);
   return cudaGetLastError();
 }
 

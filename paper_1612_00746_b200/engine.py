@@ -685,12 +685,17 @@ def enqueue_group(config: RunConfig, ens, start: int, targets, group=None):
         pur = torch.empty(npts, dtype=torch.float64, device=ens.dev)
         if npts * max(ens.count, 1) * dim * 16 <= SNAPSHOT_BYTES and ens.count:
             # the states at every point written by the same call (the resident
-            # kernel stores them from registers), then one overlap pass per point
+            # kernel stores them from registers), then the overlap sums of all
+            # points in one launch set (one pass per point across ranks, which
+            # gathers every rank's states)
             snap = torch.empty((npts, ens.count, dim), dtype=torch.complex128, device=ens.dev)
             ens.evolve_observe(start, targets[-1] - start, config.post_rate, acc, snap=snap)
-            for k in range(npts):
-                st = sharding.gather_states(snap[k], group)
-                ens.handle.overlap_sumsq(st, st.shape[0], st, st.shape[0], pur[k:k + 1])
+            if sharding.is_collective(group):
+                for k in range(npts):
+                    st = sharding.gather_states(snap[k], group)
+                    ens.handle.overlap_sumsq(st, st.shape[0], st, st.shape[0], pur[k:k + 1])
+            else:
+                ens.handle.overlap_sumsq_points(snap, ens.count, npts, ens.count * dim, pur)
         else:
             prev = start
             for k, t in enumerate(targets):

@@ -107,6 +107,7 @@ SIGNATURES = {
     "ctqw_fixed_to_double": (ctypes.c_int, [_P, _P, _P, _P]),
     "ctqw_observe_reduce": (ctypes.c_int, [_P, _P, _D, _P, _P, _P, _P]),
     "ctqw_overlap_sumsq": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
+    "ctqw_overlap_sumsq_points": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _P]),
     "ctqw_packed_gram": (ctypes.c_int, [_P, _I64, _I64, _D, _P, _I32, _P]),
     "ctqw_set_initial": (ctypes.c_int, [_P, _P]),
     "ctqw_evolve_observe": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, ctypes.POINTER(Stepper),
@@ -388,6 +389,11 @@ class Handle:
     def overlap_sumsq(self, a, count_a: int, b, count_b: int, out):
         self._check(self.lib.ctqw_overlap_sumsq(self._h, _ptr(a), int(count_a), _ptr(b),
                                                 int(count_b), _ptr(out), self.stream))
+
+    def overlap_sumsq_points(self, stacks, count: int, npoints: int, point_stride: int, out):
+        """out[p] = sum_{i,j} |<a_i|a_j>|^2 for the stack at stacks + p * point_stride."""
+        self._check(self.lib.ctqw_overlap_sumsq_points(self._h, _ptr(stacks), int(count), int(npoints),
+                                                       int(point_stride), _ptr(out), self.stream))
 
 
 def packed_gram(stack, count: int, packed, scale: float):

@@ -212,6 +212,11 @@ def merge_segment_stats(per_rank):
     return merged
 
 
+def is_collective(group=None) -> bool:
+    """Do collectives run for ``group`` (more than one rank, or forced)?"""
+    return _collective(group)
+
+
 def gather_states(local, group=None):
     """Concatenate every rank's state shard (used only for purity)."""
     import torch
@@ -233,5 +238,5 @@ def gather_states(local, group=None):
     return torch.view_as_complex(out) if local.is_complex() else out
 
 
-__all__ = ["world_info", "shard_bounds", "all_shards", "allreduce_sum_", "allreduce_int_", "gather_objects",
+__all__ = ["world_info", "is_collective", "shard_bounds", "all_shards", "allreduce_sum_", "allreduce_int_", "gather_objects",
            "gather_stats", "pack_stats", "unpack_stats", "merge_segment_stats", "gather_states"]

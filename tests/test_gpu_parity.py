@@ -689,6 +689,43 @@ def test_packed_gram_rejects_empty_stack(pkg):
         native.packed_gram(dev, 0, out, 1.0)
 
 
+@pytest.mark.parametrize("count,npoints", [(1, 1), (12, 3), (37, 5), (100, 10)])
+def test_overlap_sumsq_points_matches_per_point_and_numpy(pkg, count, npoints):
+    """ctqw_overlap_sumsq_points (every point of a schedule group in one
+    launch set) gives each point the same bits as a separate
+    ctqw_overlap_sumsq call, and sum |<a_i|a_j>|^2 to 1e-13 relative
+    (observables.py:86-91 via the Gram of the states)."""
+    n = 64
+    h = make_handle(2, n)
+    dim = n * n
+    rng = np.random.default_rng(count * 100 + npoints)
+    snap = rng.standard_normal((npoints, count, dim)) + 1j * rng.standard_normal((npoints, count, dim))
+    snap /= np.linalg.norm(snap, axis=2, keepdims=True)
+    dev = torch.as_tensor(snap, device="cuda:0").contiguous()
+    got = torch.empty(npoints, dtype=torch.float64, device="cuda:0")
+    h.overlap_sumsq_points(dev, count, npoints, count * dim, got)
+    one = torch.empty(npoints, dtype=torch.float64, device="cuda:0")
+    for k in range(npoints):
+        h.overlap_sumsq(dev[k], count, dev[k], count, one[k:k + 1])
+    assert got.cpu().numpy().tobytes() == one.cpu().numpy().tobytes()
+    for k in range(npoints):
+        g = snap[k].conj() @ snap[k].T
+        ref = float(np.sum(np.abs(g) ** 2))
+        assert abs(float(got[k]) - ref) <= 1e-13 * ref
+
+
+def test_overlap_sumsq_points_rejects_bad_arguments(pkg):
+    h = make_handle(2, 8)
+    dev = torch.zeros((2, 3, 64), dtype=torch.complex128, device="cuda:0")
+    out = torch.empty(2, dtype=torch.float64, device="cuda:0")
+    with pytest.raises(pkg.ConfigurationError):
+        h.overlap_sumsq_points(dev, 3, 0, 3 * 64, out)
+    with pytest.raises(pkg.ConfigurationError):
+        h.overlap_sumsq_points(dev, 3, 2, 3 * 64 - 1, out)
+    with pytest.raises(pkg.ConfigurationError):
+        h.overlap_sumsq_points(dev, 0, 2, 3 * 64, out)
+
+
 # ---------------------------------------------------------------------------
 # general lattices (q > 1, k_half > 1, open boundaries): generic kernels
 
