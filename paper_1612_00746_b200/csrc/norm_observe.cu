@@ -244,14 +244,31 @@ __global__ void joint_sums_kernel(const double* __restrict__ diag, int64_t dim, 
   }
 }
 
+// The block partials of the two joint sums, reduced by one warp in a fixed
+// order (lane l takes partials l, l+32, ..., then a shuffle tree): the same
+// bits on the per-point and the batched path.
+__device__ __forceinline__ void joint_final_warp(const double* __restrict__ pp, int nparts, double& s1,
+                                                 double& s2) {
+  const int lane = threadIdx.x & 31;
+  s1 = 0.0;
+  s2 = 0.0;
+  for (int i = lane; i < nparts; i += 32) {
+    s1 += pp[2 * i];
+    s2 += pp[2 * i + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_down_sync(0xffffffffu, s1, o);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+}
+
 __global__ void joint_final_kernel(const double* __restrict__ partial, int nparts,
                                    double* scalars) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s1 = 0.0, s2 = 0.0;
-  for (int i = 0; i < nparts; ++i) {
-    s1 += partial[2 * i];
-    s2 += partial[2 * i + 1];
-  }
+  if (blockIdx.x != 0) return;
+  double s1, s2;
+  joint_final_warp(partial, nparts, s1, s2);
+  if (threadIdx.x != 0) return;
   scalars[0] = s1;
   scalars[1] = s2;
   // participation ratio 1 / sum (p/S1)^2 = S1^2 / S2  (observables.py:94-101)
@@ -261,48 +278,59 @@ __global__ void joint_final_kernel(const double* __restrict__ partial, int npart
 }
 
 // sum_{i,j} |<a_i|b_j>|^2 : 32 x 32 tiles of the overlap matrix G = A^H B,
-// each thread a 2 x 2 sub-block, D split over `ksplit` blocks per tile
-// (partial G tiles summed in a fixed order afterwards -> deterministic).
+// 64 threads per tile, each a 4 x 4 register block (rows ty + 8u, columns
+// tx + 8v: a warp's row reads are broadcasts and its column reads one
+// 128-byte wavefront, 64 DFMA per 8 shared loads), D split over `ksplit`
+// blocks per tile (partial G tiles summed in a fixed order afterwards ->
+// deterministic).  blockIdx.z is the collection point.
 constexpr int kOT = 32;   // overlap tile
 constexpr int kOK = 16;   // D chunk staged through shared memory
+constexpr int kOThreads = 64;
+constexpr int kOReg = 16;  // accumulators per thread
 
-__global__ void __launch_bounds__(256) overlap_partial_kernel(const double2* __restrict__ a, int64_t ra,
-                                                              const double2* __restrict__ b, int64_t rb,
-                                                              int64_t dim, int same, int64_t ntj,
-                                                              int64_t kspan, int64_t pstride,
-                                                              double2* __restrict__ gpart) {
+__global__ void __launch_bounds__(kOThreads) overlap_partial_kernel(const double2* __restrict__ a, int64_t ra,
+                                                                    const double2* __restrict__ b, int64_t rb,
+                                                                    int64_t dim, int same, int64_t ntj,
+                                                                    int64_t kspan, int64_t pstride,
+                                                                    double2* __restrict__ gpart) {
   __shared__ double2 sa[kOK][kOT + 1];
   __shared__ double2 sb[kOK][kOT + 1];
-  // blockIdx.z: collection point (stacks pstride elements apart)
   a += (int64_t)blockIdx.z * pstride;
   b += (int64_t)blockIdx.z * pstride;
-  gpart += (int64_t)blockIdx.z * gridDim.x * gridDim.y * 256 * 4;
+  gpart += (int64_t)blockIdx.z * gridDim.x * gridDim.y * kOThreads * kOReg;
   const int64_t tile = blockIdx.x;
   const int64_t ti = tile / ntj, tj = tile % ntj;
   const int ks = blockIdx.y;
   const int tid = threadIdx.x;
   if (same && tj < ti) return;
-  const int li = (tid / 16) * 2, lj = (tid % 16) * 2;
-  double2 g[2][2];
-  for (int u = 0; u < 2; ++u)
-    for (int v = 0; v < 2; ++v) g[u][v] = make_double2(0.0, 0.0);
+  const int ty = tid >> 3, tx = tid & 7;
+  double2 g[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) g[u][v] = make_double2(0.0, 0.0);
   const int64_t klo = ks * kspan;
   const int64_t khi = klo + kspan < dim ? klo + kspan : dim;
   for (int64_t k0 = klo; k0 < khi; k0 += kOK) {
-    for (int e = tid; e < kOK * kOT; e += 256) {
+#pragma unroll
+    for (int e = tid; e < kOK * kOT; e += kOThreads) {
       const int kk = e % kOK, rr = e / kOK;
       const int64_t gi = ti * kOT + rr, gj = tj * kOT + rr, gk = k0 + kk;
       sa[kk][rr] = (gi < ra && gk < khi) ? a[gi * dim + gk] : make_double2(0.0, 0.0);
       sb[kk][rr] = (gj < rb && gk < khi) ? b[gj * dim + gk] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-#pragma unroll
+#pragma unroll 4
     for (int kk = 0; kk < kOK; ++kk) {
-      double2 av[2], bv[2];
-      for (int u = 0; u < 2; ++u) av[u] = sa[kk][li + u];
-      for (int v = 0; v < 2; ++v) bv[v] = sb[kk][lj + v];
-      for (int u = 0; u < 2; ++u)
-        for (int v = 0; v < 2; ++v) {
+      double2 av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = sa[kk][ty + 8 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = sb[kk][tx + 8 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
           // conj(a) * b
           g[u][v].x = fma(av[u].x, bv[v].x, fma(av[u].y, bv[v].y, g[u][v].x));
           g[u][v].y = fma(av[u].x, bv[v].y, fma(-av[u].y, bv[v].x, g[u][v].y));
@@ -310,15 +338,17 @@ __global__ void __launch_bounds__(256) overlap_partial_kernel(const double2* __r
     }
     __syncthreads();
   }
-  double2* out = gpart + ((tile * gridDim.y + ks) * 256 + tid) * 4;
-  for (int u = 0; u < 2; ++u)
-    for (int v = 0; v < 2; ++v) out[u * 2 + v] = g[u][v];
+  double2* out = gpart + ((tile * gridDim.y + ks) * kOThreads + tid) * kOReg;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) out[u * 4 + v] = g[u][v];
 }
 
-__global__ void __launch_bounds__(256) overlap_finish_kernel(const double2* __restrict__ gpart, int ksplit,
-                                                             int same, int64_t ntj, double* partial) {
+__global__ void __launch_bounds__(kOThreads) overlap_finish_kernel(const double2* __restrict__ gpart, int ksplit,
+                                                                   int same, int64_t ntj, double* partial) {
   __shared__ double red[32];
-  gpart += (int64_t)blockIdx.y * gridDim.x * ksplit * 256 * 4;
+  gpart += (int64_t)blockIdx.y * gridDim.x * ksplit * kOThreads * kOReg;
   partial += (int64_t)blockIdx.y * gridDim.x;
   const int64_t tile = blockIdx.x;
   const int64_t ti = tile / ntj, tj = tile % ntj;
@@ -328,9 +358,9 @@ __global__ void __launch_bounds__(256) overlap_finish_kernel(const double2* __re
     return;
   }
   double sq = 0.0;
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < kOReg; ++q) {
     double2 g = make_double2(0.0, 0.0);
-    for (int ks = 0; ks < ksplit; ++ks) g = cadd(g, gpart[((tile * ksplit + ks) * 256 + tid) * 4 + q]);
+    for (int ks = 0; ks < ksplit; ++ks) g = cadd(g, gpart[((tile * ksplit + ks) * kOThreads + tid) * kOReg + q]);
     sq += norm2(g);
   }
   const double tot = block_sum(sq, red);
@@ -505,13 +535,9 @@ __global__ void joint_sums_points_kernel(const double* __restrict__ diag, int64_
 
 __global__ void joint_final_points_kernel(const double* __restrict__ partial, int nparts, double* out,
                                           int64_t out_stride, int n) {
+  double s1, s2;
+  joint_final_warp(partial + (int64_t)blockIdx.x * 2 * nparts, nparts, s1, s2);
   if (threadIdx.x != 0) return;
-  const double* pp = partial + (int64_t)blockIdx.x * 2 * nparts;
-  double s1 = 0.0, s2 = 0.0;
-  for (int i = 0; i < nparts; ++i) {
-    s1 += pp[2 * i];
-    s2 += pp[2 * i + 1];
-  }
   double* o = out + (int64_t)blockIdx.x * out_stride + n;
   o[0] = s1;
   o[1] = s2;
@@ -552,7 +578,7 @@ int64_t overlap_parts(int64_t ra, int64_t rb, bool same) {
 
 int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim, int64_t npoints) {
   const int64_t tiles = overlap_parts(ra, rb, same);
-  const int64_t per = ((tiles + 1) & ~int64_t(1)) + tiles * overlap_ksplit(ra, rb, same, dim) * 256 * 4 * 2;
+  const int64_t per = ((tiles + 1) & ~int64_t(1)) + tiles * overlap_ksplit(ra, rb, same, dim) * kOThreads * kOReg * 2;
   return per * npoints;
 }
 
@@ -571,10 +597,10 @@ cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b,
   double2* gpart = reinterpret_cast<double2*>(scratch + ((tiles * npoints + 1) & ~int64_t(1)));
   int64_t kspan = (dim + ks - 1) / ks;
   kspan = ((kspan + kOK - 1) / kOK) * kOK;
-  overlap_partial_kernel<<<dim3((unsigned)tiles, (unsigned)ks, (unsigned)npoints), 256, 0, s>>>(
+  overlap_partial_kernel<<<dim3((unsigned)tiles, (unsigned)ks, (unsigned)npoints), kOThreads, 0, s>>>(
       a, ra, b, rb, dim, same ? 1 : 0, ntj, kspan, pstride, gpart);
-  overlap_finish_kernel<<<dim3((unsigned)tiles, (unsigned)npoints), 256, 0, s>>>(gpart, ks, same ? 1 : 0, ntj,
-                                                                                 partial);
+  overlap_finish_kernel<<<dim3((unsigned)tiles, (unsigned)npoints), kOThreads, 0, s>>>(gpart, ks, same ? 1 : 0,
+                                                                                       ntj, partial);
   sum_kernel<<<(unsigned)npoints, 1024, 0, s>>>(partial, tiles, out);
   return cudaGetLastError();
 }
