@@ -389,7 +389,9 @@ __device__ __forceinline__ void load_plane(const Plane3Args& a, const T3& T, con
   const uint32_t bar = bar_addr(slot);
   const uint32_t dst0 = s_u32(smem3) + (uint32_t)slot * kPlaneB;
   const int plane = (int)(P.g0 + y);
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  // no proxy fence here: the slot's generic accesses are reads, ordered by the
+  // barrier every thread passed (a rescale's in-place writes fence themselves,
+  // wait_plane)
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kPlaneB) : "memory");
 #pragma unroll
   for (int t = 0; t < kTR; ++t) {
