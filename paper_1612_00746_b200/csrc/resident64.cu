@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
   double* hv = reinterpret_cast<double*>(sm64 + (RK4 ? 3 : 2) * kPlane64);
   double* sv = hv + kN64;
   double* red = sv + kN64;
+  // Taylor with a collection (ctqw_evolve_observe): the point's limbs [3][N^2]
+  unsigned long long* lbuf = reinterpret_cast<unsigned long long*>(red + 16);
   constexpr bool HORN = !RK4 && !EXACT;
 
   const int64_t r = a.r_base + blockIdx.x;
@@ -240,17 +242,41 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
       if (rel % a.post_rate == 0 || gs == a.final_step) {
         const long long idx = (rel + a.post_rate - 1) / a.post_rate - 1;
         unsigned long long* o = a.obs + idx * 3 * (int64_t)kPlane64;
+        if constexpr (!RK4) {
+          // staged through shared memory, so a warp's reductions cover 256
+          // contiguous bytes (8 sectors) instead of 32 sectors: the L2 sector
+          // operations, not the adds, bound the scattered form (measured
+          // 6.5 -> 2 us per point at R = 100).  The previous point's reads of
+          // lbuf finished before the step's application barriers.
 #pragma unroll
-        for (int i = 0; i < kB64; ++i)
+          for (int i = 0; i < kB64; ++i) {
+            long long l[3][kB64];
 #pragma unroll
-          for (int q = 0; q < kB64; ++q) {
-            long long l2, l1, l0;
-            fixed_split(norm2_rn(cur[i][q]), l2, l1, l0);
-            const int al = (y0 + i) * kN64 + x0 + q;
-            atomicAdd(o + al, (unsigned long long)l2);
-            atomicAdd(o + kPlane64 + al, (unsigned long long)l1);
-            atomicAdd(o + 2 * kPlane64 + al, (unsigned long long)l0);
+            for (int q = 0; q < kB64; ++q) fixed_split(norm2_rn(cur[i][q]), l[0][q], l[1][q], l[2][q]);
+            const int al = (y0 + i) * kN64 + x0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              ulonglong2* d = reinterpret_cast<ulonglong2*>(lbuf + c * kPlane64 + al);
+              d[0] = make_ulonglong2((unsigned long long)l[c][0], (unsigned long long)l[c][1]);
+              d[1] = make_ulonglong2((unsigned long long)l[c][2], (unsigned long long)l[c][3]);
+            }
           }
+          __syncthreads();
+#pragma unroll 4
+          for (int f = tid; f < 3 * kPlane64; f += kThreads64) atomicAdd(o + f, lbuf[f]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < kB64; ++i)
+#pragma unroll
+            for (int q = 0; q < kB64; ++q) {
+              long long l2, l1, l0;
+              fixed_split(norm2_rn(cur[i][q]), l2, l1, l0);
+              const int al = (y0 + i) * kN64 + x0 + q;
+              atomicAdd(o + al, (unsigned long long)l2);
+              atomicAdd(o + kPlane64 + al, (unsigned long long)l1);
+              atomicAdd(o + 2 * kPlane64 + al, (unsigned long long)l0);
+            }
+        }
         if (a.snap) {
           double2* sp = a.snap + (idx * a.count + r) * (int64_t)kPlane64;
 #pragma unroll
@@ -269,11 +295,14 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
 
 template <bool RK4, bool SITE, bool EXACT, bool ZD, int NAPP>
 cudaError_t launch64(const Res64Args& a, int64_t count, cudaStream_t s) {
-  constexpr size_t smem = (size_t)(RK4 ? 3 : 2) * kPlane64 * sizeof(double2) + (2 * kN64 + 16) * sizeof(double);
+  constexpr size_t smem0 = (size_t)(RK4 ? 3 : 2) * kPlane64 * sizeof(double2) + (2 * kN64 + 16) * sizeof(double);
+  constexpr size_t smem_obs = smem0 + (RK4 ? 0 : (size_t)3 * kPlane64 * sizeof(unsigned long long));
+  static_assert(smem_obs <= 227 * 1024, "resident64 shared memory");
+  const size_t smem = a.obs ? smem_obs : smem0;
   auto kern = resident64_kernel<RK4, SITE, EXACT, ZD, NAPP>;
   static DeviceOnce once;
   if (once.first()) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_obs);
     if (e != cudaSuccess) return e;
   }
   Res64Args b = a;
