@@ -66,6 +66,11 @@ __device__ __forceinline__ int zo(int y, int x) { return y * kN64 + (x ^ ((x >> 
 __device__ __forceinline__ constexpr bool rim(int i, int q) { return i == 0 || i == kB64 - 1 || q == 0 || q == kB64 - 1; }
 __device__ __forceinline__ int w64(int v) { return v & (kN64 - 1); }
 
+__device__ __forceinline__ void st_v4(double2* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+               : "memory");
+}
+
 template <bool RK4, bool SITE, bool EXACT, bool ZD, int NAPP>
 __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_constant__ Res64Args a) {
   extern __shared__ __align__(16) double2 sm64[];
@@ -279,10 +284,11 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
         }
         if (a.snap) {
           double2* sp = a.snap + (idx * a.count + r) * (int64_t)kPlane64;
+          // 32-byte stores: whole L2 sectors
 #pragma unroll
           for (int i = 0; i < kB64; ++i)
 #pragma unroll
-            for (int q = 0; q < kB64; ++q) sp[(y0 + i) * kN64 + x0 + q] = cur[i][q];
+            for (int q = 0; q < kB64; q += 2) st_v4(sp + (y0 + i) * kN64 + x0 + q, cur[i][q], cur[i][q + 1]);
         }
       }
     }
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
 #pragma unroll
   for (int i = 0; i < kB64; ++i)
 #pragma unroll
-    for (int q = 0; q < kB64; ++q) gpsi[(y0 + i) * kN64 + x0 + q] = acc[i][q];
+    for (int q = 0; q < kB64; q += 2) st_v4(gpsi + (y0 + i) * kN64 + x0 + q, acc[i][q], acc[i][q + 1]);
 }
 
 template <bool RK4, bool SITE, bool EXACT, bool ZD, int NAPP>
