@@ -203,15 +203,33 @@ int validate_stepper(ctqw_ctx* h, const ctqw_stepper_t* st) {
   return CTQW_OK;
 }
 
+// integrator label of a kernel variant string
+const char* integ_label(const StepScalars& sc) {
+  return sc.rk4_horner ? "rk4=taylor4" : sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor";
+}
+
 StepScalars scalars_for(const ctqw_ctx* h, const ctqw_stepper_t* st) {
   StepScalars sc{};
   sc.backend = st->backend;
   // coeff = -1j*dt/hbar has real part 0 and imaginary part -dt/hbar; the
   // Taylor recursion multiplies by coeff/j (propagators.py:185,191).
   const double c = -st->dt / h->model.hbar;
-  if (st->backend == CTQW_BACKEND_TAYLOR) {
-    sc.order = st->order;
-    for (int j = 1; j <= st->order; ++j) sc.ci[j - 1] = c / (double)j;
+  // For a Hamiltonian constant over the step, classic RK4 is exactly the
+  // degree-4 Taylor polynomial: (k1 + 2k2 + 2k3 + k4)/6 = A + A^2/2 + A^3/6 +
+  // A^4/24 applied to psi (A = coeff*H; the reference's own tests assert
+  // RK4 == Taylor-4, test_propagators.py:112-119).  Exact mode keeps the
+  // reference's stage arithmetic bit for bit; FMA mode only promises 1e-12, so
+  // it evaluates that polynomial in Horner form with the Taylor kernels (12
+  // instead of 14 FP64 instructions per amplitude and stage, no stage stash).
+  // CTQW_RK4_STAGES=1 keeps the stage form (A/B and the stage kernels' tests).
+  const char* stages = std::getenv("CTQW_RK4_STAGES");
+  const bool horner = st->backend == CTQW_BACKEND_RK4 && !st->exact &&
+                      !(stages && stages[0] != '\0' && std::strcmp(stages, "0") != 0);
+  if (st->backend == CTQW_BACKEND_TAYLOR || horner) {
+    if (horner) sc.backend = CTQW_BACKEND_TAYLOR;
+    sc.rk4_horner = horner ? 1 : 0;
+    sc.order = horner ? 4 : st->order;
+    for (int j = 1; j <= sc.order; ++j) sc.ci[j - 1] = c / (double)j;
   } else {
     sc.order = 4;
     sc.ci[0] = c;
@@ -810,8 +828,7 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
     const bool r64 = uses_resident64(h, sc);
     h->stream_kernel = r64 ? "resident64_kernel" : "resident_kernel";
     std::snprintf(h->variant, sizeof(h->variant), "%s<%s,order=%d,site=%d,exact=%d,N=%d>", h->stream_kernel,
-                  sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", sc.order, coef.site != nullptr ? 1 : 0,
-                  exact ? 1 : 0, h->n);
+                  integ_label(sc), sc.order, coef.site != nullptr ? 1 : 0, exact ? 1 : 0, h->n);
     // a pending initial state: resident64 reads it directly, the strip kernel
     // needs the stack materialised
     const double2* init = h->initial;
@@ -877,7 +894,7 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
       // (plane3: without site noise)
       const int dg = ((use_band4 && nn > 0 && zd) || (use_plane3 && zd && coef.site == nullptr)) ? 0 : 2;
       std::snprintf(h->variant, sizeof(h->variant), "%s<%s,napp=%d,site=%d,exact=%d,NN=%d,dg=%d>", h->stream_kernel,
-                    sc.backend == CTQW_BACKEND_RK4 ? "rk4" : "taylor", napp, coef.site != nullptr ? 1 : 0,
+                    integ_label(sc), napp, coef.site != nullptr ? 1 : 0,
                     exact ? 1 : 0, nn, dg);
     }
     const int nparts = use_plane3 ? plane3_parts()
@@ -935,8 +952,8 @@ int evolve_impl(ctqw_ctx* h, double* psi_dev, double* work_dev, int64_t count, i
   }
   // generic path: in place on psi; work = term buffer A, library scratch B, C
   h->stream_kernel = sc.backend == CTQW_BACKEND_TAYLOR ? "taylor_order_kernel" : "rk4_stage_kernel";
-  std::snprintf(h->variant, sizeof(h->variant), "%s<order=%d,site=%d,exact=%d>", h->stream_kernel, sc.order,
-                coef.site != nullptr ? 1 : 0, exact ? 1 : 0);
+  std::snprintf(h->variant, sizeof(h->variant), "%s<%sorder=%d,site=%d,exact=%d>", h->stream_kernel,
+                sc.rk4_horner ? "rk4=taylor4," : "", sc.order, coef.site != nullptr ? 1 : 0, exact ? 1 : 0);
   rc = ensure_scratch(h, count * h->dim);
   if (rc) return rc;
   const int nparts = generic_parts(h->dim);

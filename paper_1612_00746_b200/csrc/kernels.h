@@ -42,6 +42,7 @@ struct StepScalars {
   int backend;  // 0 taylor, 1 rk4
   int order;    // Taylor order (applications per step); 4 for RK4
   double ci[kMaxTaylorOrder];  // imaginary part of coeff/j, j = 1..order (taylor); ci[0] = coeff (rk4)
+  int rk4_horner;  // 1: an FMA-mode RK4 step run as the Taylor-4 kernels (the same polynomial)
 };
 
 int generic_parts(int64_t dim);

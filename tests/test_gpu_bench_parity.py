@@ -9,6 +9,8 @@ Tolerances: bit-exact in exact mode without renormalisations; 1e-13 absolute
 once rescales happen; FMA mode within 1e-12 (the bench's arithmetic).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -32,15 +34,26 @@ def _check(h, st, m, n, B, backend, dt, steps, variant_exact, variant_fma, expec
         np.testing.assert_array_equal(mine, ref)
     else:
         assert np.abs(mine - ref).max() <= 1e-13
-    fma, fstats = run_evolve(h, psi0, B, steps, stepper(backend, 4, dt, exact=False))
-    assert h.step_variant() == variant_fma
-    assert fstats.corrections == ostats.corrections
-    assert np.abs(fma - ref).max() <= 1e-12
-    # per-realization squared norms agree with the oracle's to rounding (norm
-    # conservation is judged against the oracle's norm)
-    n2 = (np.abs(fma) ** 2).sum(axis=1)
-    n2_ref = (np.abs(ref) ** 2).sum(axis=1)
-    assert np.abs(n2 - n2_ref).max() <= 1e-12
+    # FMA-mode RK4 runs as the Taylor-4 kernels (the same polynomial, api.cu
+    # scalars_for); CTQW_RK4_STAGES=1 keeps the stage form, checked too
+    forms = [(variant_fma.replace("<rk4,", "<rk4=taylor4,"), None)]
+    if backend == "rk4":
+        forms.append((variant_fma, "1"))
+    for var, stages in forms:
+        if stages:
+            os.environ["CTQW_RK4_STAGES"] = stages
+        try:
+            fma, fstats = run_evolve(h, psi0, B, steps, stepper(backend, 4, dt, exact=False))
+        finally:
+            os.environ.pop("CTQW_RK4_STAGES", None)
+        assert h.step_variant() == var
+        assert fstats.corrections == ostats.corrections
+        assert np.abs(fma - ref).max() <= 1e-12
+        # per-realization squared norms agree with the oracle's to rounding (norm
+        # conservation is judged against the oracle's norm)
+        n2 = (np.abs(fma) ** 2).sum(axis=1)
+        n2_ref = (np.abs(ref) ** 2).sum(axis=1)
+        assert np.abs(n2 - n2_ref).max() <= 1e-12
 
 
 BAND4_BENCH = [
@@ -154,9 +167,19 @@ def test_resident64_variants_match_oracle(pkg, case):
     ref, ostats = orc.evolve_segment(st, psi0.copy(), 0, steps, dt, 1.0, backend, order)
     assert (ostats.corrections > 0) == rescale
     site = int(target in ("onsite", "both"))
-    for exact in (True, False):
-        mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, order, dt, exact=exact))
-        assert h.step_variant() == f"resident64_kernel<{backend},order={order},site={site},exact={int(exact)},N=64>"
+    # (exact, CTQW_RK4_STAGES, integrator label): FMA-mode RK4 runs as
+    # Taylor-4 unless the stage form is pinned
+    forms = [(True, None, backend), (False, None, "rk4=taylor4" if backend == "rk4" else backend)]
+    if backend == "rk4":
+        forms.append((False, "1", "rk4"))
+    for exact, stages, label in forms:
+        if stages:
+            os.environ["CTQW_RK4_STAGES"] = stages
+        try:
+            mine, stats = run_evolve(h, psi0, B, steps, stepper(backend, order, dt, exact=exact))
+        finally:
+            os.environ.pop("CTQW_RK4_STAGES", None)
+        assert h.step_variant() == f"resident64_kernel<{label},order={order},site={site},exact={int(exact)},N=64>"
         assert stats.corrections == ostats.corrections and stats.event_count == ostats.event_count
         if exact and ostats.event_count == 0:
             np.testing.assert_array_equal(mine, ref)
