@@ -1,9 +1,10 @@
 // Row-marching streaming step kernel for m = 2, four columns per thread,
 // lag-1 stage pipeline, persistent balanced row-block schedule.
 //
-// Why another band kernel.  The one- and two-column kernels (step_band.cu,
-// step_band2.cu) are bound by shared memory (ncu: 1.5-2.6 wavefronts per
-// element-step, L1/TEX 66-85 % busy) and by latency at 8-16 warps/SM.  Here
+// Why four columns.  The one- and two-column kernels of round 1 (retired;
+// DESIGN.md section 4 has their measurements) were bound by shared memory
+// (ncu: 1.5-2.6 wavefronts per element-step, L1/TEX 66-85 % busy) and by
+// latency at 8-16 warps/SM.  Here
 // each thread owns four adjacent columns, so per stencil application it
 // publishes only its two edge values and reads one value from each
 // neighbouring thread: 8 B/element of shared-memory traffic per application
@@ -24,11 +25,12 @@
 //   stage k:  t_k(j-k+1) from t_{k-1}(j-k), t_{k-1}(j-k+1), t_{k-1}(j-k+2)
 //   last:     out(j-n+1) = acc + t_n -> HBM, |out|^2 -> norm partial
 //
-// psi rows stream in through an 8-row cp.async ring: lanes fetch contiguous
-// 16-byte chunks (coalesced) and write them XOR-swizzled
-// (chunk c -> c ^ ((c >> 3) & 7)) so that a thread's four-column reads and
-// the neighbour reads are bank-conflict free.  Finished rows leave from
-// registers as two 256-bit stores per thread.
+// psi rows stream in through an 8-row ring, XOR-swizzled (chunk c ->
+// c ^ ((c >> 3) & 7)) so that a thread's four-column reads and the neighbour
+// reads are bank-conflict free: one TMA box per row (128B swizzle, mbarrier
+// per slot) at the compile-time sizes N = 256/512/1024, lane-contiguous
+// 16-byte cp.async chunks otherwise.  Finished rows leave from registers as
+// two 256-bit stores per thread.
 //
 // Schedule.  The realization x row space is cut into blocks of kRB rows.  A
 // persistent grid (CTAs resident per SM x SMs) takes equal contiguous runs
