@@ -340,6 +340,60 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
   }
 }
 
+// FMA-mode Horner stage in two halves around the split CTA barrier: the
+// terms from the thread's own registers (plane r-1, r+1 and the in-block
+// in-plane neighbours) before the wait, the four in-plane neighbours other
+// warps published last iteration after it (same terms as apply3, FMA order).
+template <bool SITE, bool ZD>
+__device__ __forceinline__ void apply3_own(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
+                                           const Quad& dn, Quad& h) {
+  const double2 h0 = smem3[kHopOff + r];
+  const double s0 = SITE ? site_tab()[r] : 0.0;
+  const double2 h1a = smem3[kHopOff + T.x1a], h1b = smem3[kHopOff + T.x1a + 1];
+  const double h1[3] = {h1a.x, h1a.y, h1b.y};
+  const double* h2 = T.h2;
+  const double* s2 = T.s2;
+  double s1[2] = {0.0, 0.0};
+  if (SITE) {
+    s1[0] = site_tab()[T.x1a];
+    s1[1] = site_tab()[T.x1a + 1];
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int a = q >> 1, b = q & 1;
+    const int x1 = T.x1a + a, x2 = T.x2a + b;
+    double2 v;
+    if constexpr (ZD) {
+      v = rmul(h0.x, up.c[q]);
+    } else {
+      const int cc = (r == x1) + (r == x2) + (x1 == x2);
+      double v0 = K.base[cc];
+      if (SITE) v0 = __dadd_rn(v0, __dadd_rn(__dadd_rn(s0, s1[a]), s2[b]));
+      v = madd<false>(rmul(v0, mid.c[q]), h0.x, up.c[q]);
+    }
+    // the in-block neighbours: x1 +move for a = 0, -move for a = 1; x2 likewise
+    v = a == 0 ? madd<false>(v, h1[1], mid.c[2 + b]) : madd<false>(v, h1[a], mid.c[b]);
+    v = b == 0 ? madd<false>(v, h2[1], mid.c[2 * a + 1]) : madd<false>(v, h2[b], mid.c[2 * a]);
+    h.c[q] = madd<false>(v, h0.y, dn.c[q]);
+  }
+}
+
+__device__ __forceinline__ void apply3_nb(const T3& T, int r, const Nb& nb, const Quad& h, double ci, Quad& out,
+                                          const Quad& psi) {
+  const double2 h1a = smem3[kHopOff + T.x1a], h1b = smem3[kHopOff + T.x1a + 1];
+  const double h1[3] = {h1a.x, h1a.y, h1b.y};
+  const double* h2 = T.h2;
+  (void)r;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int a = q >> 1, b = q & 1;
+    double2 v = h.c[q];
+    v = a == 1 ? madd<false>(v, h1[1 + a], nb.x1p[b]) : madd<false>(v, h1[a], nb.x1m[b]);
+    v = b == 1 ? madd<false>(v, h2[1 + b], nb.x2p[a]) : madd<false>(v, h2[b], nb.x2m[a]);
+    out.c[q] = ifma(psi.c[q], ci, v);
+  }
+}
+
 __device__ __forceinline__ void store3(const T3& T, Piece3& P, int rr, const Quad& o, double& nrm) {
   // in place, output planes 0..kWrap-1 would overwrite psi planes the march
   // reads again at its end (as planes N..N+3): park them
@@ -554,6 +608,10 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   // iteration, an mbarrier per iteration parity), and every CTA of the
   // cluster has consumed the halo rows this iteration's pushes overwrite
   // (the relaxed cluster barrier).
+  // FMA-mode Horner: stage 2's terms from this thread's registers before the
+  // wait too (its neighbour terms need the other warps' rows, after it)
+  Quad h2own;
+  if constexpr (HORN) apply3_own<SITE, ZD>(T, a.k, wrap3(j - 1), R.old[1], mid1, nt, h2own);
   if (i > 0) {
     const int G = P.it0 + i - 1;
     mbar_wait3(bar_addr(kSplit3 + (G & 1)), (uint32_t)(G >> 1) & 1u);
@@ -571,7 +629,15 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   if (i < P.iters - 1) halo_push(T, 0, buf, nt);
   R.m1 = nt;
   halo_wait(T, 0, i);
-  const Quad t2 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
+  Quad t2;
+  if constexpr (HORN) {
+    apply3_nb(T, wrap3(j - 1), xch_nb(T, 0, buf ^ 1), h2own, a.ci[NAPP - 2], t2, R.acc[SM1]);
+    R.old[1] = mid1;
+    xch_put(T, 1, buf, t2);
+    if (i < P.iters - 1) halo_push(T, 1, buf, t2);
+  } else {
+    t2 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
+  }
   halo_wait(T, 1, i);
   const Quad t3 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 3>(a, T, P, R, i, j, xch_own(T, 1, buf ^ 1), t2,
                                                                   xch_nb(T, 1, buf ^ 1));
