@@ -628,7 +628,12 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   xch_put(T, 0, buf, nt);
   if (i < P.iters - 1) halo_push(T, 0, buf, nt);
   R.m1 = nt;
+  // the halo rows of all three stages were pushed during the neighbours'
+  // previous iteration: wait for them together, so the stages below run as
+  // one block of straight-line code
   halo_wait(T, 0, i);
+  halo_wait(T, 1, i);
+  halo_wait(T, 2, i);
   Quad t2;
   if constexpr (HORN) {
     apply3_nb(T, wrap3(j - 1), xch_nb(T, 0, buf ^ 1), h2own, a.ci[NAPP - 2], t2, R.acc[SM1]);
@@ -638,10 +643,8 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   } else {
     t2 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
   }
-  halo_wait(T, 1, i);
   const Quad t3 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 3>(a, T, P, R, i, j, xch_own(T, 1, buf ^ 1), t2,
                                                                   xch_nb(T, 1, buf ^ 1));
-  halo_wait(T, 2, i);
   plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, NAPP>(a, T, P, R, i, j, xch_own(T, NAPP - 2, buf ^ 1), t3,
                                                      xch_nb(T, NAPP - 2, buf ^ 1));
   if (RK4) R.acc[PH] = t;
