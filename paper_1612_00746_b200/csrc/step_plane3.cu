@@ -133,6 +133,7 @@ struct T3 {
   int u, v, c;          // x1 pair, x2 pair, cluster rank (x1 band)
   int x1a, x2a;         // first owned x1 / x2
   double h2[3];         // hop[x2a-1], hop[x2a], hop[x2a+1] (per lane: kept in registers)
+  double h1[3];         // hop[x1a-1], hop[x1a], hop[x1a+1] (warp-uniform)
   double s2[2];         // site[x2a + b]
   uint32_t up_nb;       // shared::cluster address of smem3 in rank c-1 (x1 row above the band)
   uint32_t dn_nb;       // ... in rank c+1 (x1 row below the band)
@@ -289,12 +290,12 @@ template <bool EXACT, bool SITE, bool HORN = false, bool RAW = false, bool ZD = 
 __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
                                        const Quad& dn, const Nb& nb, double ci, Quad& out,
                                        const Quad* psi = nullptr) {
-  // couplings re-read from the shared table (hop2[y] = (hop[y-1], hop[y]))
-  // at every application: holding them in registers spills
+  // particle-0 couplings of plane r from the shared table (hop2[y] =
+  // (hop[y-1], hop[y])); the x1 / x2 couplings of the thread's block live in
+  // registers (T.h1, T.h2: +1.5 % over re-reading them per application)
   const double2 h0 = smem3[kHopOff + r];
   const double s0 = SITE ? site_tab()[r] : 0.0;
-  const double2 h1a = smem3[kHopOff + T.x1a], h1b = smem3[kHopOff + T.x1a + 1];
-  const double h1[3] = {h1a.x, h1a.y, h1b.y};  // hop[x1a-1], hop[x1a], hop[x1a+1] (warp-uniform)
+  const double* h1 = T.h1;
   const double* h2 = T.h2;
   const double* s2 = T.s2;
   double s1[2] = {0.0, 0.0};
@@ -349,8 +350,7 @@ __device__ __forceinline__ void apply3_own(const T3& T, const StencilConst& K, i
                                            const Quad& dn, Quad& h) {
   const double2 h0 = smem3[kHopOff + r];
   const double s0 = SITE ? site_tab()[r] : 0.0;
-  const double2 h1a = smem3[kHopOff + T.x1a], h1b = smem3[kHopOff + T.x1a + 1];
-  const double h1[3] = {h1a.x, h1a.y, h1b.y};
+  const double* h1 = T.h1;
   const double* h2 = T.h2;
   const double* s2 = T.s2;
   double s1[2] = {0.0, 0.0};
@@ -380,8 +380,7 @@ __device__ __forceinline__ void apply3_own(const T3& T, const StencilConst& K, i
 
 __device__ __forceinline__ void apply3_nb(const T3& T, int r, const Nb& nb, const Quad& h, double ci, Quad& out,
                                           const Quad& psi) {
-  const double2 h1a = smem3[kHopOff + T.x1a], h1b = smem3[kHopOff + T.x1a + 1];
-  const double h1[3] = {h1a.x, h1a.y, h1b.y};
+  const double* h1 = T.h1;
   const double* h2 = T.h2;
   (void)r;
 #pragma unroll
@@ -727,6 +726,8 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     }
 #pragma unroll
     for (int t = 0; t < 3; ++t) T.h2[t] = hop[wrap3(T.x2a - 1 + t)];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) T.h1[t] = hop[wrap3(T.x1a - 1 + t)];
 #pragma unroll
     for (int t = 0; t < 2; ++t) T.s2[t] = SITE ? sg[T.x2a + t] : 0.0;
     P.s = a.scl ? a.scl[r] : 1.0;
