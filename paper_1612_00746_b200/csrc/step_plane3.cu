@@ -177,6 +177,7 @@ struct Regs3 {
   Quad acc[3];     // running sums, slot = row mod 3 (relative)
   Quad up;
   Quad m1;         // stage-1 output of the last iteration (own block), instead of re-reading it
+  double2 h0w[3];  // hop2[] of the planes stage 1 read, slot = iteration phase (stages 2-4 reuse them)
   double nrm;
 };
 
@@ -287,13 +288,12 @@ __device__ __forceinline__ void xch_put(const T3& T, int k, int buf, const Quad&
 // out = i*ci*(H z), or with HORN psi + i*ci*(H z) (Horner-form Taylor, as
 // step_band4.cu).
 template <bool EXACT, bool SITE, bool HORN = false, bool RAW = false, bool ZD = false>
-__device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
-                                       const Quad& dn, const Nb& nb, double ci, Quad& out,
+__device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r, double2 h0, const Quad& up,
+                                       const Quad& mid, const Quad& dn, const Nb& nb, double ci, Quad& out,
                                        const Quad* psi = nullptr) {
   // particle-0 couplings of plane r from the shared table (hop2[y] =
   // (hop[y-1], hop[y])); the x1 / x2 couplings of the thread's block live in
   // registers (T.h1, T.h2: +1.5 % over re-reading them per application)
-  const double2 h0 = smem3[kHopOff + r];
   const double s0 = SITE ? site_tab()[r] : 0.0;
   const double* h1 = T.h1;
   const double* h2 = T.h2;
@@ -346,9 +346,8 @@ __device__ __forceinline__ void apply3(const T3& T, const StencilConst& K, int r
 // in-plane neighbours) before the wait, the four in-plane neighbours other
 // warps published last iteration after it (same terms as apply3, FMA order).
 template <bool SITE, bool ZD>
-__device__ __forceinline__ void apply3_own(const T3& T, const StencilConst& K, int r, const Quad& up, const Quad& mid,
-                                           const Quad& dn, Quad& h) {
-  const double2 h0 = smem3[kHopOff + r];
+__device__ __forceinline__ void apply3_own(const T3& T, const StencilConst& K, int r, double2 h0, const Quad& up,
+                                           const Quad& mid, const Quad& dn, Quad& h) {
   const double s0 = SITE ? site_tab()[r] : 0.0;
   const double* h1 = T.h1;
   const double* h2 = T.h2;
@@ -497,7 +496,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 // middle one.  Returns the stage's output (the next stage's dn).
 template <int NAPP, bool RK4, bool SITE, bool EXACT, bool ZD, bool SC, int PH, int K>
 __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, Piece3& P, Regs3<NAPP>& R, int i,
-                                             int j, const Quad& mid, const Quad& dn, const Nb& nb) {
+                                             int j, const Quad& mid, const Quad& dn, const Nb& nb, double2 h0) {
   constexpr double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
   constexpr int s0 = ((PH - K + 1) % 3 + 3) % 3;  // acc slot of plane j-K+1
   const int buf = i & 1;
@@ -508,7 +507,7 @@ __device__ __forceinline__ Quad plane3_stage(const Plane3Args& a, const T3& T, P
   constexpr bool RKF = RK4 && !EXACT && !SITE;
   const double ci = RK4 ? a.ci[0] : (HORN ? a.ci[NAPP - K] : a.ci[K - 1]);
   Quad tk;
-  apply3<EXACT, SITE, HORN, RKF, ZD>(T, a.k, rr, R.old[K - 1], mid, dn, nb, ci, tk, &R.acc[s0]);
+  apply3<EXACT, SITE, HORN, RKF, ZD>(T, a.k, rr, h0, R.old[K - 1], mid, dn, nb, ci, tk, &R.acc[s0]);
   R.old[K - 1] = mid;
   Quad nk;
   if constexpr (RKF) {
@@ -576,7 +575,13 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   constexpr bool HORN = !RK4 && !EXACT;
   constexpr bool RKF = RK4 && !EXACT && !SITE;
   Quad t;
-  apply3<EXACT, SITE, HORN, RKF, ZD>(T, a.k, r, R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
+  // the plane's couplings: stage 1 loads them, stages 2-4 reuse them in the
+  // following iterations (slot = iteration phase; stage 4's plane j-3 leaves
+  // the window as plane j enters it)
+  const double2 h0_4 = R.h0w[PH];
+  R.h0w[PH] = smem3[kHopOff + r];
+  apply3<EXACT, SITE, HORN, RKF, ZD>(T, a.k, r, R.h0w[PH], R.up, psi, dn, nb, HORN ? a.ci[NAPP - 1] : a.ci[0], t,
+                                     &psi);
   const Quad mid1 = R.m1;  // t1 (arg1) of plane j-1
   Quad nt;
   if constexpr (RKF) {
@@ -610,7 +615,7 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   // FMA-mode Horner: stage 2's terms from this thread's registers before the
   // wait too (its neighbour terms need the other warps' rows, after it)
   Quad h2own;
-  if constexpr (HORN) apply3_own<SITE, ZD>(T, a.k, wrap3(j - 1), R.old[1], mid1, nt, h2own);
+  if constexpr (HORN) apply3_own<SITE, ZD>(T, a.k, wrap3(j - 1), R.h0w[(PH + 2) % 3], R.old[1], mid1, nt, h2own);
   if (i > 0) {
     const int G = P.it0 + i - 1;
     mbar_wait3(bar_addr(kSplit3 + (G & 1)), (uint32_t)(G >> 1) & 1u);
@@ -640,12 +645,13 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
     xch_put(T, 1, buf, t2);
     if (i < P.iters - 1) halo_push(T, 1, buf, t2);
   } else {
-    t2 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1));
+    t2 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 2>(a, T, P, R, i, j, mid1, nt, xch_nb(T, 0, buf ^ 1),
+                                                             R.h0w[(PH + 2) % 3]);
   }
   const Quad t3 = plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, 3>(a, T, P, R, i, j, xch_own(T, 1, buf ^ 1), t2,
-                                                                  xch_nb(T, 1, buf ^ 1));
+                                                                  xch_nb(T, 1, buf ^ 1), R.h0w[(PH + 1) % 3]);
   plane3_stage<NAPP, RK4, SITE, EXACT, ZD, SC, PH, NAPP>(a, T, P, R, i, j, xch_own(T, NAPP - 2, buf ^ 1), t3,
-                                                     xch_nb(T, NAPP - 2, buf ^ 1));
+                                                     xch_nb(T, NAPP - 2, buf ^ 1), h0_4);
   if (RK4) R.acc[PH] = t;
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_addr(kSplit3 + ((P.it0 + i) & 1)))
                : "memory");
@@ -761,6 +767,8 @@ __global__ void __launch_bounds__(kThreads3, 1) plane3_kernel(const __grid_const
     for (int w = 0; w < 3; ++w)
 #pragma unroll
       for (int q = 0; q < 4; ++q) R.acc[w].c[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < 3; ++w) R.h0w[w] = make_double2(0.0, 0.0);
     R.nrm = 0.0;
     plane3_loop<NAPP, RK4, SITE, EXACT, ZD, false>(a, T, P, R, iters);  // ring tiles arrive pre-scaled
     cluster_wait();   // completes the last iteration's arrive
