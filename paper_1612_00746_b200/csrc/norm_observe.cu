@@ -345,26 +345,148 @@ __global__ void __launch_bounds__(kOThreads) overlap_partial_kernel(const double
     for (int v = 0; v < 4; ++v) out[u * 4 + v] = g[u][v];
 }
 
-__global__ void __launch_bounds__(kOThreads) overlap_finish_kernel(const double2* __restrict__ gpart, int ksplit,
-                                                                   int same, int64_t ntj, double* partial) {
+// one thread per G entry of the tile (kOThreads x kOReg = 1024), summing the
+// D split in order with coalesced loads
+__global__ void __launch_bounds__(kOThreads * kOReg) overlap_finish_kernel(const double2* __restrict__ gpart,
+                                                                           int ksplit, int same, int64_t ntj,
+                                                                           double* partial) {
   __shared__ double red[32];
-  gpart += (int64_t)blockIdx.y * gridDim.x * ksplit * kOThreads * kOReg;
+  constexpr int kE = kOThreads * kOReg;
+  gpart += (int64_t)blockIdx.y * gridDim.x * ksplit * kE;
   partial += (int64_t)blockIdx.y * gridDim.x;
   const int64_t tile = blockIdx.x;
   const int64_t ti = tile / ntj, tj = tile % ntj;
-  const int tid = threadIdx.x;
+  const int e = threadIdx.x;
   if (same && tj < ti) {
-    if (tid == 0) partial[tile] = 0.0;
+    if (e == 0) partial[tile] = 0.0;
     return;
   }
+  double2 g = make_double2(0.0, 0.0);
+  for (int ks = 0; ks < ksplit; ++ks) g = cadd(g, gpart[(tile * ksplit + ks) * kE + e]);
+  const double tot = block_sum(norm2(g), red);
+  if (e == 0) partial[tile] = (same && tj > ti) ? 2.0 * tot : tot;
+}
+
+// Small stacks (one stack against itself, R <= kTriMaxR, the purity case):
+// the upper triangle of G = A A^H in 4 x 4 register blocks, every block
+// (bi <= bj) one thread, so neither the padding of R to a tile nor the lower
+// half of the diagonal tiles is computed (R = 100: 325 blocks, half the work
+// of the 32 x 32 tiles).  Grid (ksplit, point); D split over ksplit CTAs in a
+// fixed way (independent of the point count), partial blocks summed in order.
+// Shared memory holds a 16-wide k chunk as [row mod 4][k][row / 4], so the
+// column reads of a warp (consecutive bj) are contiguous.
+constexpr int kTriMaxR = 124;     // 31 x 32 / 2 = 496 blocks
+constexpr int kTriK = 16;
+constexpr int kTriThreads = 512;  // 128 registers per thread
+
+__device__ __forceinline__ void cpa16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+
+__global__ void __launch_bounds__(kTriThreads, 1) overlap_tri_kernel(const double2* __restrict__ a, int64_t R,
+                                                                     int64_t dim, int nb, int nbp, int nblk,
+                                                                     int64_t kspan, int64_t pstride,
+                                                                     double2* __restrict__ gpart) {
+  extern __shared__ double2 tri_st[];  // two buffers of [4][kTriK][nbp]
+  const int bufsz = 4 * kTriK * nbp;
+  a += (int64_t)blockIdx.y * pstride;
+  gpart += ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * nblk * 16;
+  const int tid = threadIdx.x;
+  // rows R .. 4 nb - 1 are never staged: zero them once (both buffers)
+  for (int e = tid; e < 2 * bufsz; e += blockDim.x) tri_st[e] = make_double2(0.0, 0.0);
+  // my block: row-major over the upper triangle
+  int bi = 0, rem = tid;
+  while (bi < nb && rem >= nb - bi) {
+    rem -= nb - bi;
+    ++bi;
+  }
+  const bool active = tid < nblk;
+  const int bj = active ? bi + rem : 0;
+  if (!active) bi = 0;
+  double2 g[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) g[u][v] = make_double2(0.0, 0.0);
+  const int64_t klo = (int64_t)blockIdx.x * kspan;
+  const int64_t khi = klo + kspan < dim ? klo + kspan : dim;
+  const int nchunk = (int)((khi - klo + kTriK - 1) / kTriK);
+  __syncthreads();
+  // k chunks staged with cp.async, double-buffered: chunk c + 1 is in flight
+  // while chunk c is multiplied
+  auto stage = [&](int c) {
+    double2* st = tri_st + (c & 1) * bufsz;
+    const int64_t k0 = klo + (int64_t)c * kTriK;
+    for (int e = tid; e < kTriK * R; e += blockDim.x) {
+      const int kk = e % kTriK, r = e / kTriK;
+      const int64_t gk = k0 + kk;
+      const bool ok = gk < khi;
+      cpa16_zfill(st + ((r & 3) * kTriK + kk) * nbp + (r >> 2), a + r * dim + (ok ? gk : klo), ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  stage(0);
+  for (int c = 0; c < nchunk; ++c) {
+    if (c + 1 < nchunk) {
+      stage(c + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double2* st = tri_st + (c & 1) * bufsz;
+    if (active) {
+#pragma unroll 4
+      for (int kk = 0; kk < kTriK; ++kk) {
+        double2 av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = st[(u * kTriK + kk) * nbp + bi];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) bv[v] = st[(v * kTriK + kk) * nbp + bj];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            // conj(a) * b
+            g[u][v].x = fma(av[u].x, bv[v].x, fma(av[u].y, bv[v].y, g[u][v].x));
+            g[u][v].y = fma(av[u].x, bv[v].y, fma(-av[u].y, bv[v].x, g[u][v].y));
+          }
+      }
+    }
+    __syncthreads();  // buffer c & 1 is restaged for chunk c + 2
+  }
+  if (active) {
+    double2* out = gpart + (int64_t)tid * 16;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) out[u * 4 + v] = g[u][v];
+  }
+}
+
+// sum over the D split, |.|^2, weight 2 off the diagonal blocks: one thread
+// per G entry (coalesced over the [ks][block][16] partials), one partial per
+// 256 entries and point
+__global__ void __launch_bounds__(256) overlap_tri_finish_kernel(const double2* __restrict__ gpart, int ksplit,
+                                                                 int nb, int nblk, double* partial) {
+  __shared__ double red[32];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = nblk * 16;
+  const double2* gp = gpart + (int64_t)blockIdx.y * ksplit * n;
   double sq = 0.0;
-  for (int q = 0; q < kOReg; ++q) {
+  if (e < n) {
     double2 g = make_double2(0.0, 0.0);
-    for (int ks = 0; ks < ksplit; ++ks) g = cadd(g, gpart[((tile * ksplit + ks) * kOThreads + tid) * kOReg + q]);
-    sq += norm2(g);
+    for (int ks = 0; ks < ksplit; ++ks) g = cadd(g, gp[(int64_t)ks * n + e]);
+    int bi = 0, rem = e >> 4;
+    while (bi < nb && rem >= nb - bi) {
+      rem -= nb - bi;
+      ++bi;
+    }
+    sq = (rem == 0 ? 1.0 : 2.0) * norm2(g);  // bj == bi: the diagonal block holds both halves
   }
   const double tot = block_sum(sq, red);
-  if (tid == 0) partial[tile] = (same && tj > ti) ? 2.0 * tot : tot;
+  if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
 
 __global__ void sum_kernel(const double* __restrict__ partial, int64_t nparts, double* out) {
@@ -576,7 +698,18 @@ int64_t overlap_parts(int64_t ra, int64_t rb, bool same) {
   return ti * tj;
 }
 
+static bool overlap_tri(int64_t ra, int64_t rb, bool same) { return same && ra == rb && ra <= kTriMaxR; }
+static int tri_nb(int64_t r) { return (int)((r + 3) / 4); }
+static int tri_ksplit(int64_t dim) {
+  int64_t ks = dim / 64;
+  return (int)(ks < 1 ? 1 : (ks > 64 ? 64 : ks));
+}
+
 int64_t overlap_scratch_doubles(int64_t ra, int64_t rb, bool same, int64_t dim, int64_t npoints) {
+  if (overlap_tri(ra, rb, same)) {
+    const int64_t nb = tri_nb(ra), nblk = nb * (nb + 1) / 2, chunks = (nblk * 16 + 255) / 256;
+    return npoints * (((chunks + 1) & ~int64_t(1)) + (int64_t)tri_ksplit(dim) * nblk * 16 * 2);
+  }
   const int64_t tiles = overlap_parts(ra, rb, same);
   const int64_t per = ((tiles + 1) & ~int64_t(1)) + tiles * overlap_ksplit(ra, rb, same, dim) * kOThreads * kOReg * 2;
   return per * npoints;
@@ -589,6 +722,29 @@ cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b,
                                  cudaStream_t s, int64_t npoints, int64_t pstride) {
   if (npoints < 1 || npoints > 65535) return cudaErrorInvalidValue;
   const bool same = (a == b) && (ra == rb);
+  if (overlap_tri(ra, rb, same)) {
+    if (overlap_scratch_doubles(ra, rb, same, dim, npoints) > scratch_cap) return cudaErrorInvalidValue;
+    const int nb = tri_nb(ra), nbp = nb | 1, nblk = nb * (nb + 1) / 2, chunks = (nblk * 16 + 255) / 256;
+    const int ks = tri_ksplit(dim);
+    int64_t kspan = (dim + ks - 1) / ks;
+    kspan = ((kspan + kTriK - 1) / kTriK) * kTriK;
+    const int ksn = (int)((dim + kspan - 1) / kspan);  // CTAs with work
+    double* partial = scratch;  // [P][chunks]
+    double2* gpart = reinterpret_cast<double2*>(scratch + ((chunks * npoints + 1) & ~int64_t(1)));
+    const int threads = ((nblk + 31) / 32) * 32;
+    const size_t smem = (size_t)2 * 4 * kTriK * nbp * sizeof(double2);
+    static DeviceOnce once;
+    if (once.first()) {
+      const cudaError_t e = cudaFuncSetAttribute(overlap_tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(2 * 4 * kTriK * ((kTriMaxR + 3) / 4 | 1) * sizeof(double2)));
+      if (e != cudaSuccess) return e;
+    }
+    overlap_tri_kernel<<<dim3((unsigned)ksn, (unsigned)npoints), threads, smem, s>>>(a, ra, dim, nb, nbp, nblk, kspan,
+                                                                                     pstride, gpart);
+    overlap_tri_finish_kernel<<<dim3((unsigned)chunks, (unsigned)npoints), 256, 0, s>>>(gpart, ksn, nb, nblk, partial);
+    sum_kernel<<<(unsigned)npoints, 1024, 0, s>>>(partial, chunks, out);
+    return cudaGetLastError();
+  }
   const int64_t ntj = (rb + kOT - 1) / kOT;
   const int64_t tiles = overlap_parts(ra, rb, same);
   const int ks = overlap_ksplit(ra, rb, same, dim);
@@ -599,8 +755,8 @@ cudaError_t launch_overlap_sumsq(const double2* a, int64_t ra, const double2* b,
   kspan = ((kspan + kOK - 1) / kOK) * kOK;
   overlap_partial_kernel<<<dim3((unsigned)tiles, (unsigned)ks, (unsigned)npoints), kOThreads, 0, s>>>(
       a, ra, b, rb, dim, same ? 1 : 0, ntj, kspan, pstride, gpart);
-  overlap_finish_kernel<<<dim3((unsigned)tiles, (unsigned)npoints), kOThreads, 0, s>>>(gpart, ks, same ? 1 : 0,
-                                                                                       ntj, partial);
+  overlap_finish_kernel<<<dim3((unsigned)tiles, (unsigned)npoints), kOThreads * kOReg, 0, s>>>(gpart, ks, same ? 1 : 0,
+                                                                                               ntj, partial);
   sum_kernel<<<(unsigned)npoints, 1024, 0, s>>>(partial, tiles, out);
   return cudaGetLastError();
 }

@@ -689,7 +689,7 @@ def test_packed_gram_rejects_empty_stack(pkg):
         native.packed_gram(dev, 0, out, 1.0)
 
 
-@pytest.mark.parametrize("count,npoints", [(1, 1), (12, 3), (37, 5), (100, 10)])
+@pytest.mark.parametrize("count,npoints", [(1, 1), (12, 3), (37, 5), (100, 10), (124, 2), (125, 2), (150, 2)])
 def test_overlap_sumsq_points_matches_per_point_and_numpy(pkg, count, npoints):
     """ctqw_overlap_sumsq_points (every point of a schedule group in one
     launch set) gives each point the same bits as a separate
