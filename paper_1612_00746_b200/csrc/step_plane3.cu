@@ -56,6 +56,11 @@ constexpr int kNblk3 = kN3 / kPB;    // norm blocks per realization per CTA
 constexpr int kRowB = kN3 * 16;      // bytes per x1 row (128 complex)
 constexpr int kWrap = 4;             // planes re-read at the end of a full-ring march (NAPP)
 constexpr int kPlaneB = kTR * kRowB; // ring bytes per plane
+// Per-iteration single-thread duties (TMA issue, barrier arming, norm flush)
+// go to a thread of an interior warp (u = 1): the edge warps already push
+// and await the halo rows, and every warp waits for the slowest at the CTA
+// barrier.
+constexpr int kDuty3 = 64;
 
 struct Plane3Args {
   CUtensorMap tmap;  // psi_in: (16 doubles, 16 lines, x1, count*N planes), box = one x1 row
@@ -416,7 +421,7 @@ __device__ __forceinline__ void store3(const T3& T, Piece3& P, int rr, const Qua
 // after the iteration's cluster arrive, so thread 0 adds them up only after
 // the next arrive/wait pair: pend -> pend2 -> flushed.
 __device__ __forceinline__ void flush_blk3(const T3& T, Piece3& P, int blk) {
-  if (blk >= 0 && threadIdx.x == 0) {
+  if (blk >= 0 && threadIdx.x == kDuty3) {
     const double* red = red_tab() + (blk & 1) * 8;
     double b = 0.0;
     for (int w = 0; w < kThreads3 / 32; ++w) b += red[w];
@@ -435,7 +440,7 @@ __device__ __forceinline__ void flush3(const T3& T, Piece3& P, bool all = false)
 
 // TMA: the ten x1 rows (x1a_band - 1 .. +8, wrapped) of psi plane y into slot.
 __device__ __forceinline__ void load_plane(const Plane3Args& a, const T3& T, const Piece3& P, int rho) {
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x != kDuty3) return;
   const int y = wrap3(P.j0 - 1 + rho);
   const int slot = rho % kRing3;
   const uint32_t bar = bar_addr(slot);
@@ -625,7 +630,7 @@ __device__ __forceinline__ void plane3_iter(const Plane3Args& a, const T3& T, Pi
   if (i + pref3<RK4>() + 1 <= P.last_rho) load_plane(a, T, P, i + pref3<RK4>() + 1);
   // arm the barriers that count this iteration's incoming halo pushes (their
   // previous phase, iteration i-2's pushes, was awaited last iteration)
-  if (i < P.iters - 1 && threadIdx.x == 0) {
+  if (i < P.iters - 1 && threadIdx.x == kDuty3) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) mbar_arm3(full_bar(k, buf), 2 * kN3 * 16);
   }
