@@ -121,6 +121,12 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
   const bool diag_block = g == p;  // amplitudes with x0 == x1 lie in the diagonal blocks
   constexpr double c16 = 1.0 / 6.0, c13 = 1.0 / 3.0;
   RealStat* st_r = a.stats + r;
+  // the realization's statistics live in thread 0's registers for the whole
+  // segment (written back at the end): the per-step norm decision then needs
+  // no global load, which would hold warp 0 -- and at the next barrier every
+  // warp -- for a memory round trip per step
+  RealStat st_l;
+  if (tid == 0) st_l = *st_r;
   EventRec* ev_r = a.events + r * kMaxEvents;
   int b = 0;  // buffer holding the current stage input
 
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
     const long long step_no = a.first_step + step + 1;
     if (tid == 0) {  // statistics, events and the failure flag
       int failed = 0;
-      norm_decide(n2, step_no, a.pol, st_r, ev_r, &failed);
+      norm_decide(n2, step_no, a.pol, &st_l, ev_r, &failed);
       if (failed) atomicMin(reinterpret_cast<unsigned long long*>(a.fail), (unsigned long long)step_no);
     }
     const double dev = fabs(n2 - 1.0);
@@ -293,6 +299,7 @@ __global__ void __launch_bounds__(kThreads64, 1) resident64_kernel(const __grid_
       }
     }
   }
+  if (tid == 0) *st_r = st_l;
 #pragma unroll
   for (int i = 0; i < kB64; ++i)
 #pragma unroll
