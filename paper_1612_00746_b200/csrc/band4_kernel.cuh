@@ -376,9 +376,11 @@ __device__ __forceinline__ void band4_stage(const Band4Args& a, const Geo4<NN>& 
   // the row's couplings: loaded by stage 1 K-1 iterations ago (slot =
   // its phase), stage NAPP's row leaves the window in this iteration (hw4).
   // Without on-site noise only: the on-site variants spill with the window
-  // (measured -8.5 % at N = 1024, +3.5 % tunnelling-only at N = 256)
-  const double2 hp = SITE ? smem4[L::hop2(g) + rr]
-                          : (K == NAPP && NAPP >= 4 ? hw4 : R.hw[((PH - K + 1) % 3 + 3) % 3]);
+  // (measured -8.5 % at N = 1024, +3.5 % tunnelling-only at N = 256), and
+  // the RK4 stage form (exact mode) spills with it too
+  constexpr bool HWIN = !SITE && !RK4;  // RK4 (exact / stage form) spills with it
+  const double2 hp = !HWIN ? smem4[L::hop2(g) + rr]
+                           : (K == NAPP && NAPP >= 4 ? hw4 : R.hw[((PH - K + 1) % 3 + 3) % 3]);
   apply4<EXACT, SITE, DG, !RK4 || RKF, HORN, RKF>(T, a.k, rr, hp, SITE ? L::site(g)[rr] : 0.0,
                                            R.w[K - 1][sm], R.w[K - 1][s0], R.w[K - 1][sp], lf, rt, ci, tk,
                                            &R.acc[s0]);
@@ -525,9 +527,9 @@ __device__ __forceinline__ void band4_iter(const Band4Args& a, const Geo4<NN>& g
   constexpr bool HORN = horner4<NAPP, RK4, EXACT>();
   constexpr bool RKF = rk4fma<RK4, EXACT>();
   Row4 t;
-  const double2 hw4 = SITE ? double2() : R.hw[PH];  // row j-3 (stage 4's) leaves the window, row j enters
+  const double2 hw4 = (SITE || RK4) ? double2() : R.hw[PH];  // row j-3 (stage 4's) leaves the window, row j enters
   const double2 hp1 = smem4[L::hop2(g) + r];
-  if constexpr (!SITE) R.hw[PH] = hp1;
+  if constexpr (!SITE && !RK4) R.hw[PH] = hp1;
   apply4<EXACT, SITE, DG, !RK4 || RKF, HORN, RKF>(T, a.k, r, hp1, SITE ? L::site(g)[r] : 0.0, R.up, psi,
                                            dn, lf, rt, HORN ? a.ci[NAPP - 1] : a.ci[0], t, &psi);
   if constexpr (NAPP == 1) {
