@@ -83,8 +83,58 @@ class InitialStateSpec:
             object.__setattr__(self, "positions", tuple(int(x) for x in self.positions))
 
 
+# pinned host buffers for the initial-state upload, by dimension: [tensor,
+# nonzero indices written last (None: unknown / dense), event of the last
+# upload from it]
+_PINNED: dict = {}
+
+
+def _pinned_initial(dim: int) -> list:
+    import torch
+
+    pool = _PINNED.get(dim)
+    if pool:
+        buf = pool.pop()
+        if buf[2] is not None:
+            buf[2].synchronize()
+        return buf
+    return [torch.empty(dim, dtype=torch.complex128, pin_memory=torch.cuda.is_available()), None, None]
+
+
+def _fill_pinned(buf: list, entries) -> None:
+    arr = buf[0].numpy()
+    if isinstance(entries, np.ndarray):
+        arr[:] = entries
+        buf[1] = None
+        return
+    if buf[1] is None:
+        arr[:] = 0
+    else:
+        arr[list(buf[1])] = 0
+    for k, v in entries.items():
+        arr[k] = v
+    buf[1] = tuple(entries.keys())
+
+
+class _Entries(dict):
+    """The nonzero entries of a closed-form initial state (psi[index] = value)."""
+
+
 def build_initial_state(spec: InitialStateSpec, space: JointSpace) -> np.ndarray:
     """Unit-norm joint state (ensemble.py:147-216), complex128 on the host."""
+    entries = initial_state_entries(spec, space)
+    if isinstance(entries, np.ndarray):
+        return entries
+    psi = np.zeros(space.dim, dtype=np.complex128)
+    for k, v in entries.items():
+        psi[k] = v
+    return psi
+
+
+def initial_state_entries(spec: InitialStateSpec, space: JointSpace):
+    """build_initial_state's state: the dense vector for custom amplitudes,
+    else its few nonzero entries (an ``_Entries`` dict), so a pinned upload
+    buffer can be updated in place instead of rewritten."""
     n, m = space.lattice.n_sites, space.m
     kind = spec.kind
     if kind == KIND_AUTO:
@@ -99,7 +149,7 @@ def build_initial_state(spec: InitialStateSpec, space: JointSpace) -> np.ndarray
         if norm == 0:
             raise ConfigurationError("custom vector has zero norm")
         return amps / norm
-    psi = np.zeros(space.dim, dtype=np.complex128)
+    psi = _Entries()
     if kind == KIND_SINGLE_SITE:
         if m != 1:
             raise ConfigurationError("single_site describes one particle only")
@@ -421,8 +471,15 @@ class EnsembleState:
         self.handle.bind(self.hop, self.site, self.count, self.topology.n_links)
         self.handle.telegraph_enable(self.dynamic and self.count > 0)
         del noise
-        psi0 = build_initial_state(config.initial, space)
-        self.psi0 = torch.as_tensor(psi0, device=self.dev)
+        # the initial state goes up from a pooled pinned buffer (asynchronous
+        # copy on the stream); closed-form states only rewrite their few
+        # nonzero entries in it
+        self._pinned = _pinned_initial(space.dim)
+        _fill_pinned(self._pinned, initial_state_entries(config.initial, space))
+        self.psi0 = torch.empty(space.dim, dtype=torch.complex128, device=self.dev)
+        self.psi0.copy_(self._pinned[0], non_blocking=True)
+        self._pinned[2] = torch.cuda.Event()
+        self._pinned[2].record(torch.cuda.current_stream(self.dev))  # the buffer is rewritten only after this copy
         self.psi = torch.empty((max(self.count, 1), space.dim), dtype=torch.complex128, device=self.dev)
         # one buffer when the step kernel marches in place (the library keeps a
         # second one itself if another path ends up running)
@@ -516,6 +573,9 @@ class EnsembleState:
         if self.handle is not None:
             release_private_handle(self.handle)
             self.handle = None
+        if getattr(self, "_pinned", None) is not None:
+            _PINNED.setdefault(self._pinned[0].numel(), []).append(self._pinned)
+            self._pinned = None
 
 
 def _observable_rows(config, pops, pr, purity, joint):
