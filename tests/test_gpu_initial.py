@@ -55,3 +55,38 @@ def test_engine_states_before_the_first_step_are_materialised(pkg):
     s = ens.states().cpu().numpy()
     np.testing.assert_array_equal(s, np.tile(orc.product_state(2, 64), (3, 1)))
     ens.release()
+
+
+def test_pinned_initial_pool_across_state_kinds(pkg):
+    """The pooled pinned upload buffer (engine._PINNED) rewrites only the
+    nonzeros of closed-form initial states: a sequence of runs with different
+    kinds and positions on one pool gives, run for run, the rows of the same
+    runs on an empty pool."""
+    p = pkg
+    from paper_1612_00746_b200 import engine
+
+    n = 16
+    rng = np.random.default_rng(5)
+    custom = rng.standard_normal(n * n) + 1j * rng.standard_normal(n * n)
+    specs = [engine.InitialStateSpec(kind="product", positions=(3, 9)),
+             engine.InitialStateSpec(kind="symmetrized_pair", positions=(5, 6)),
+             engine.InitialStateSpec(kind="custom_vector", amplitudes=custom),
+             engine.InitialStateSpec(kind="antisymmetrized_pair", positions=(1, 12)),
+             engine.InitialStateSpec(kind="auto")]
+
+    def run(spec):
+        cfg = p.RunConfig(space=p.JointSpace(p.build_lattice([n]), 2), initial=spec,
+                          noise=p.NoiseSpec(target="both", rate=0.0), stepper=p.StepperConfig(dt=0.05),
+                          realizations=3, steps=6, post_rate=3, precision="double",
+                          observables=("populations", "participation_ratio", "joint_distribution"))
+        sinks = p.MemorySinks(keep_densities=False)
+        p.run(cfg, sinks)
+        return sinks.rows
+
+    pooled = [run(s) for s in specs]
+    fresh = []
+    for s in specs:
+        engine._PINNED.clear()
+        fresh.append(run(s))
+    assert pooled == fresh
+    assert all(pooled[k] != pooled[k + 1] for k in range(len(pooled) - 1))  # the states differ
