@@ -94,7 +94,6 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the other-arithmetic measurement")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     a = ap.parse_args()
     pre = PRESETS[a.config]
     for key in ("n", "m", "realizations", "target", "dt"):
@@ -255,19 +254,21 @@ def cpu_sample_size(n, m):
     return max(1, min(8, (4 << 20) // (16 * dim)))
 
 
-def cpu_rate(a, seconds):
-    """Wall rate of the reference pool: one warm round, then one round of as
-    many steps as fill ~``seconds``."""
+def pool_rate(a):
+    """Wall rate of the reference's own pool on this workload: one W-step
+    warm segment (spawn, imports, first touch), then the K timed steps as one
+    segment per chunk, as run() does between two collection points (the
+    values are assembled once per segment).  Both arms report this same
+    measurement, so a run carries one CPU number."""
     workers = cpu_workers()
     pool = ReferencePool(a, workers, cpu_sample_size(a.n, a.m))
     try:
-        pool.round(1)  # imports, first-touch
-        t1 = pool.round(1)
-        steps = max(1, min(500, int(round(seconds / max(t1, 1e-6)))))
-        wall = pool.round(steps)
+        pool.round(max(a.warmup, 1))
+        t_all = pool.round(a.steps)
     finally:
         pool.close()
-    return pool.realizations * steps / wall, pool, wall, steps
+    sample = f"{pool.describe()}, the K timed steps as one {a.steps}-step segment per chunk ({t_all:.1f} s wall)"
+    return a.steps * pool.realizations / t_all, pool, t_all, sample
 
 
 def cores_info(workers):
@@ -279,17 +280,8 @@ def reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    workers = cpu_workers()
-    pool = ReferencePool(a, workers, cpu_sample_size(a.n, a.m))
-    try:
-        pool.round(max(a.warmup, 1))  # spawn, imports, first touch: one W-step segment
-        # the K timed steps as one segment, as run() does between two collection
-        # points (post_rate = K): the values are assembled once per segment
-        t_all = pool.round(a.steps)
-    finally:
-        pool.close()
-    value = a.steps * pool.realizations / t_all
-    sample = f"{pool.describe()}, the K timed steps as one {a.steps}-step segment per chunk"
+    value, pool, t_all, sample = pool_rate(a)
+    workers = pool.workers
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * t_all / a.steps,
@@ -778,10 +770,8 @@ def ours(a):
 
     cpu = None  # the host-core baseline is taken on rank 0 at N = 1 only
     if rank == 0 and world == 1 and not a.no_cpu:
-        rate, pool, wall, steps = cpu_rate(a, a.cpu_seconds)
-        cpu = dict({"value": rate, "unit": UNIT, "kind": pool.kind,
-                    "sample": f"{pool.describe()}, one {steps}-step segment, {wall:.1f} s wall"},
-                   **cores_info(pool.workers))
+        rate, pool, wall, sample = pool_rate(a)
+        cpu = dict({"value": rate, "unit": UNIT, "kind": pool.kind, "sample": sample}, **cores_info(pool.workers))
 
     if rank == 0:
         line = {
